@@ -1,0 +1,344 @@
+#!/usr/bin/env python3
+"""Benchmark: simulated strategy evaluations/sec on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): Inception-v3 (125 ops, batch 64) on a
+simulated 4-node x 4-GPU topology, full-iteration task graphs, max_degree 4,
+1024 MCMC chains per GPU (weak scaling: each rank owns 1024 chains), initial
+strategies [data-parallel] + random_strategy(seed=c), Philox stream.
+A step = every chain makes ``--proposals`` Metropolis proposals, each scored
+by a full GPU re-simulation of the changed strategy (one k_mcmc launch);
+value = proposals (= strategy evaluations) of all ranks / max-over-ranks time.
+
+``--impl reference`` times the CPU restatement of the reference path
+(oracle/parasim_oracle.c: rebuild + full simulate per proposal) on all host
+threads, on a bounded sample of the same chains, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated strategy evals/sec (full+delta) at 1/2/4/8 B200 vs host-CPU ref"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--chains", type=int, default=1024, help="chains per GPU")
+    ap.add_argument("--proposals", type=int, default=16, help="proposals per chain per step")
+    ap.add_argument("--mode", default="full-iteration", choices=("forward", "full-iteration"))
+    ap.add_argument("--config", default="inception", choices=("inception", "alexnet", "resnet", "nmt", "random"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload(name):
+    import paper_1807_05358_b200 as ps
+    if name == "inception":
+        return ps.inception_v3(), ps.multi_node_topology(4, 4), 4, "Inception-v3 b64 on 4x4 GPUs (16 devices, 120 links)"
+    if name == "alexnet":
+        return ps.alexnet_like(), ps.single_node_topology(4), 4, "AlexNet-like on 1x4 GPUs"
+    if name == "resnet":
+        return ps.resnet101(), ps.multi_node_topology(16, 4), 8, "ResNet-101 b64 on 16x4 GPUs (64 devices)"
+    if name == "nmt":
+        return (ps.nmt_like(steps=40, layers=2, batch=64, hidden=1024, vocab=32768), ps.multi_node_topology(16, 4), 8,
+                "NMT-40 on 16x4 GPUs")
+    return ps.random_dag(1000, seed=1000), ps.multi_node_topology(4, 4), 4, "random DAG 1k ops on 4x4 GPUs"
+
+
+def initial_strategies(g, topo, md, first, count):
+    import paper_1807_05358_b200 as ps
+    out = []
+    for c in range(first, first + count):
+        out.append(ps.data_parallel_strategy(g, topo) if c == 0 else ps.random_strategy(g, topo, md, c))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profiled_traffic():
+    """dram bytes per k_mcmc launch from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get("k_mcmc_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(g, topo, prof, mode, md, init, seeds, seconds, threads):
+    """The oracle (CPU restatement of the reference path) on a bounded sample."""
+    from oracle.oracle_io import Oracle
+    orc = Oracle()
+    n = min(len(init), threads)
+    t0 = time.perf_counter()
+    orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], 1, md, rng_mode="philox", threads=threads)
+    per_prop = max(1e-6, (time.perf_counter() - t0))  # one full eval + one proposal per chain, in parallel
+    props = max(1, int(seconds / (2 * per_prop)))
+    t0 = time.perf_counter()
+    out = orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], props, md, rng_mode="philox", threads=threads)
+    dt = time.perf_counter() - t0
+    total = float(out["summary"][:, 2].sum())
+    # the initial full evaluation of each chain is counted as an evaluation too
+    evals = total + n
+    return {"value": evals / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n} chains x {props} proposals ({mode}, rebuild+full simulate per proposal), {dt:.1f}s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1807_05358_b200 as ps
+    g, topo, md, desc = workload(args.config)
+    prof = ps.CostProfile()
+    threads = os.cpu_count() or 1
+    init = initial_strategies(g, topo, md, 0, threads)
+    seeds = [1000003 * c for c in range(threads)]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        res = cpu_baseline(g, topo, prof, args.mode, md, init, seeds, max(2.0, args.cpu_seconds / 3), threads)
+        if i >= args.warmup:
+            vals.append(res["value"])
+    v = statistics.mean(vals)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": desc, "mode": args.mode, "max_degree": md, "chains": len(init)},
+            "cpu_baseline": {**res, "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1807_05358_b200 as ps
+    from paper_1807_05358_b200 import _native as nat
+    from paper_1807_05358_b200.lowering import lower
+    from paper_1807_05358_b200.rng import mt_state_words  # noqa: F401
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    g, topo, md, desc = workload(args.config)
+    prof = ps.CostProfile()
+    C = args.chains
+    first = rank * C
+    init = initial_strategies(g, topo, md, first, C)
+    low = lower(g, topo, prof, args.mode, max_degree=md, strategies=init, device=local)
+    info = low.info()
+    L = nat.lib()
+    maps = np.zeros((C, low.n_ops), dtype=np.int32)
+    asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+    for i, s in enumerate(init):
+        low.encode(s, maps[i], asg[i])
+    seeds = np.array([1000003 * (first + i) for i in range(C)], dtype=np.uint64)
+    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0)
+    h = ctypes.c_void_p()
+    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
+                               ctypes.byref(h)), "ps_mcmc_create")
+    stream = torch.cuda.current_stream(dev)
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    P = args.proposals
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    # first launch also scores the initial strategies (warm-up)
+    for _ in range(args.warmup):
+        nat.check(L.ps_mcmc_run(h, P, sh), "ps_mcmc_run")
+        flush.zero_()
+    torch.cuda.synchronize(dev)
+    # algorithmic bytes per evaluation: 32 B per task + 4 B per dependency, averaged
+    # over a sample of the chains' live strategies (traced on the GPU)
+    sm = np.zeros((C, low.n_ops), dtype=np.int32)
+    sa = np.zeros((C, low.n_slots), dtype=np.uint8)
+    nat.check(L.ps_mcmc_read_state(h, nat.ptr(sm), nat.ptr(sa)), "ps_mcmc_read_state")
+    tasks_edges = []
+    for i in range(0, C, max(1, C // 16)):
+        tg = ps.TaskGraph(g, topo, low.decode(sm[i], sa[i]), prof, args.mode)
+        from paper_1807_05358_b200.taskgraph import _bind
+        _bind(tg, low)
+        T = len(tg.tasks)
+        E = sum(len(t.outputs) for t in tg.tasks.values())
+        tasks_edges.append((T, E))
+    T_avg = statistics.mean(t for t, _ in tasks_edges)
+    E_avg = statistics.mean(e for _, e in tasks_edges)
+    bytes_per_eval = 32.0 * T_avg + 4.0 * E_avg
+    summ0 = (nat.PsChainSummary * C)()
+    nat.check(L.ps_mcmc_read(h, summ0, None, None, None, None), "ps_mcmc_read")
+    props0 = sum(s.proposals for s in summ0)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            nat.check(L.ps_mcmc_run(h, P, sh), "ps_mcmc_run")
+            ends[i].record(stream)
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    summ = (nat.PsChainSummary * C)()
+    nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+    evals = sum(s.proposals for s in summ) - props0
+    bad = sum(1 for s in summ if s.status != nat.PS_STATUS_OK)
+    # best strategy across chains: device argmin, then the tiny cross-GPU exchange
+    bc, bi = ctypes.c_double(), ctypes.c_int32()
+    nat.check(L.ps_mcmc_best(h, ctypes.byref(bc), ctypes.byref(bi)), "ps_mcmc_best")
+    best_local = float(bc.value)
+    t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    ev = torch.tensor([float(evals)], dtype=torch.float64, device=dev)
+    best = torch.tensor([best_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        dist.all_reduce(best, op=dist.ReduceOp.MIN)
+    total_ms = float(t_max.item())
+    all_evals = float(ev.item())
+    value = all_evals / (total_ms / 1e3)
+
+    # ---- e2e: the C-ABI with host buffers, H2D of the step's inputs and D2H of its results inside the timing
+    e2e_times = []
+    h2d = maps.nbytes + asg.nbytes + seeds.nbytes
+    best_maps = np.zeros((C, low.n_ops), dtype=np.int32)
+    best_asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+    d2h = ctypes.sizeof(nat.PsChainSummary) * C + best_maps.nbytes + best_asg.nbytes
+    e2e_evals = 0
+    for i in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        h2 = ctypes.c_void_p()
+        nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
+                                   ctypes.byref(h2)), "ps_mcmc_create")
+        nat.check(L.ps_mcmc_run(h2, P, sh), "ps_mcmc_run")
+        s2 = (nat.PsChainSummary * C)()
+        nat.check(L.ps_mcmc_read(h2, s2, nat.ptr(best_maps), nat.ptr(best_asg), None, None), "ps_mcmc_read")
+        dt = time.perf_counter() - t0
+        L.ps_mcmc_destroy(h2)
+        if i >= args.warmup:
+            e2e_times.append(dt)
+            # evaluations = the initial scoring of every chain + its proposals
+            e2e_evals += sum(s.proposals for s in s2) + C
+    e2e_t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    e2e_n = torch.tensor([float(e2e_evals)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e2e_n, op=dist.ReduceOp.SUM)
+    e2e_value = float(e2e_n.item()) / float(e2e_t.item())
+
+    peak, peak_src = measured_peak()
+    achieved = bytes_per_eval * (evals / (total_ms / 1e3)) / 1e9  # this rank's kernel, GB/s
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "mode": args.mode, "max_degree": md, "chains_per_gpu": C,
+                   "proposals_per_chain_per_step": P, "rng": "philox", "l2": "flushed between steps (256 MB write)",
+                   "tasks_per_eval": round(T_avg, 1), "deps_per_eval": round(E_avg, 1),
+                   "ready_capacity": info.ready_capacity, "overlap_entries": info.n_entries},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": profiled_traffic(),
+                     "note": f"B_eval = 32*T + 4*E = {bytes_per_eval:.0f} B (SURVEY 8d); peak {peak_src}"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+        "chain_failures": bad, "best_makespan": float(best.item()),
+    }
+    L.ps_mcmc_destroy(h)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        line["cpu_baseline"] = cpu_baseline(g, topo, prof, args.mode, md, init, [1000003 * c for c in range(C)],
+                                            args.cpu_seconds, threads)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1399 @@
+// parasim_cuda.cu -- B200 (sm_100a) strategy-evaluation path behind include/parasim.h.
+//
+// Kernels
+//   k_rows_count / k_rows_fill / k_cols_count / k_cols_fill
+//       Region-overlap tables: for every op pair and every (src degree map, dst
+//       degree map) combo, the (k, l, bytes) transfer list that _wire_pair
+//       derives for one strategy (reference taskgraph.py:154-195,
+//       partition.py:117-211), computed once per problem.  Rows (per src block
+//       k) are sorted by l; a column index (per dst block l) serves the
+//       backward pass.
+//   k_simulate_batch  one warp per candidate strategy: the task graph of the
+//       strategy is never materialised -- successors are walked straight out of
+//       the overlap tables -- and the reference's global (ready, origin) heap
+//       order (simulate.py:68-117) is reproduced exactly by a warp-wide argmin
+//       over a shared-memory ready set.  Per-queue (device / link) clocks live
+//       in shared memory.
+//   k_mcmc  persistent, one warp per chain: proposal (Philox4x32-10 or CPython
+//       MT19937 stream), in-place fragment rewrite, re-simulation, Metropolis
+//       accept, best snapshot, O(size) rollback (search.py:89-115,193-255).
+//
+// Exactness: the only floating-point operations on the simulated timeline are
+// max() and one IEEE add per task (start + exe), plus lat + bytes/bw for
+// transfers and shard/r for ring hops -- each a single correctly rounded op in
+// the reference's operand order.  Built with -fmad=false.
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include <stdint.h>
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "parasim.h"
+
+#define FULLMASK 0xffffffffu
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) return fail(PS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+enum { KIND_EDGE = 0, KIND_EDGE_BWD = 1, KIND_OP = 2, KIND_OP_BWD = 3, KIND_SYNC = 4 };
+
+struct DevProb {
+  int n_ops, n_dev, n_kinds, n_links, n_pairs, n_maps, full, n_slots, n_queues, cap;
+  const int *dev_kind, *link_of;
+  const double *link_bw, *link_lat;
+  const int *op_ndim;
+  const long long *op_dim;
+  const int *op_esize, *op_param_mask, *op_map_off, *op_nmaps_enum, *op_slot_off, *slot_op;
+  const int *op_in_off, *op_in_pairs, *op_out_off, *op_out_pairs;
+  const int *map_deg, *map_size;
+  const double *exe_fwd, *exe_bwd, *map_shard;
+  const int *map_ngroups;
+  const int *pair_src, *pair_dst, *pair_need_off, *need, *combo_off, *combo_row_off, *combo_col_off;
+  // derived on the device
+  const int *row_ent_off, *col_ent_off, *col_ent;
+  const unsigned short *ent_k, *ent_l;
+  const long long *ent_bytes;
+};
+
+__host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
+                                                               unsigned c, unsigned d) {
+  return ((unsigned long long)kind << 61) | ((unsigned long long)a << 45) | ((unsigned long long)b << 29) |
+         ((unsigned long long)c << 14) | (unsigned long long)d;
+}
+__device__ __forceinline__ unsigned key_kind(unsigned long long k) { return (unsigned)(k >> 61); }
+__device__ __forceinline__ unsigned key_a(unsigned long long k) { return (unsigned)(k >> 45) & 0xffffu; }
+__device__ __forceinline__ unsigned key_b(unsigned long long k) { return (unsigned)(k >> 29) & 0xffffu; }
+__device__ __forceinline__ unsigned key_c(unsigned long long k) { return (unsigned)(k >> 14) & 0x7fffu; }
+__device__ __forceinline__ unsigned key_d(unsigned long long k) { return (unsigned)k & 0x3fffu; }
+
+// first index in [0, n) with a[i] > x
+__device__ __forceinline__ int upper_bound(const int *a, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void block_bounds(const DevProb &P, int op, int g, int k, long long *lo, long long *hi) {
+  int nd = P.op_ndim[op];
+  for (int i = nd - 1; i >= 0; --i) {
+    int d = P.map_deg[g * PS_MAXDIM + i];
+    int c = k % d;
+    k /= d;
+    long long step = P.op_dim[op * PS_MAXDIM + i] / d;
+    lo[i] = c * step;
+    hi[i] = lo[i] + step;
+  }
+}
+
+// Bytes src block k sends to dst block l over every tensor edge of pair p
+// (taskgraph.py:168-195): sum over edges of esize * prod_dims |need ∩ block|.
+__device__ long long overlap_bytes(const DevProb &P, int p, int gs, int gd, int k, int l) {
+  int src = P.pair_src[p], dst = P.pair_dst[p];
+  long long slo[PS_MAXDIM], shi[PS_MAXDIM], dlo[PS_MAXDIM], dhi[PS_MAXDIM];
+  block_bounds(P, src, gs, k, slo, shi);
+  block_bounds(P, dst, gd, l, dlo, dhi);
+  int nd = P.op_ndim[src];
+  long long total = 0;
+  for (int e = P.pair_need_off[p]; e < P.pair_need_off[p + 1]; ++e) {
+    long long prod = P.op_esize[src];
+    bool ok = true;
+    for (int j = 0; j < nd && ok; ++j) {
+      const int *d = P.need + (e * PS_MAXDIM + j) * PS_NEED_STRIDE;
+      int od = d[1];
+      long long ext = d[2], nlo, nhi;
+      switch (d[0]) {
+        case PS_NEED_FULL: nlo = 0; nhi = ext; break;
+        case PS_NEED_IDENT: nlo = dlo[od]; nhi = dhi[od]; break;
+        case PS_NEED_WINDOW: {
+          long long stride = d[4], pad = d[5], kern = d[3];
+          nlo = dlo[od] * stride - pad;
+          nhi = (dhi[od] - 1) * stride - pad + kern;
+          if (nlo < 0) nlo = 0;
+          if (nhi > ext) nhi = ext;
+          break;
+        }
+        default: {  // CONCAT
+          long long off = d[6];
+          long long a = dlo[od] > off ? dlo[od] : off;
+          long long b = dhi[od] < off + ext ? dhi[od] : off + ext;
+          if (a >= b) { ok = false; nlo = nhi = 0; break; }
+          nlo = a - off;
+          nhi = b - off;
+        }
+      }
+      if (!ok) break;
+      long long size = P.op_dim[src * PS_MAXDIM + j];
+      if (nlo < 0) nlo = 0;
+      if (nhi > size) nhi = size;
+      long long a = nlo > slo[j] ? nlo : slo[j];
+      long long b = nhi < shi[j] ? nhi : shi[j];
+      if (a >= b) { ok = false; break; }
+      prod *= (b - a);
+    }
+    if (ok) total += prod;
+  }
+  return total;
+}
+
+struct ComboRef { int p, gs, gd, ns, nd; };
+
+__device__ __forceinline__ ComboRef combo_ref(const DevProb &P, int c) {
+  ComboRef r;
+  r.p = upper_bound(P.combo_off, P.n_pairs + 1, c) - 1;
+  int src = P.pair_src[r.p], dst = P.pair_dst[r.p];
+  int nmd = P.op_map_off[dst + 1] - P.op_map_off[dst];
+  int local = c - P.combo_off[r.p];
+  r.gs = P.op_map_off[src] + local / nmd;
+  r.gd = P.op_map_off[dst] + local % nmd;
+  r.ns = P.map_size[r.gs];
+  r.nd = P.map_size[r.gd];
+  return r;
+}
+
+__global__ void k_rows(DevProb P, int n_rows, int n_combos, int *row_count, int *row_off_fill) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  int c = upper_bound(P.combo_row_off, n_combos + 1, r) - 1;
+  int k = r - P.combo_row_off[c];
+  ComboRef cr = combo_ref(P, c);
+  if (row_off_fill == nullptr) {
+    int cnt = 0;
+    for (int l = 0; l < cr.nd; ++l) cnt += overlap_bytes(P, cr.p, cr.gs, cr.gd, k, l) > 0;
+    row_count[r] = cnt;
+  } else {
+    int pos = row_off_fill[r];
+    for (int l = 0; l < cr.nd; ++l) {
+      long long b = overlap_bytes(P, cr.p, cr.gs, cr.gd, k, l);
+      if (b > 0) {
+        const_cast<unsigned short *>(P.ent_k)[pos] = (unsigned short)k;
+        const_cast<unsigned short *>(P.ent_l)[pos] = (unsigned short)l;
+        const_cast<long long *>(P.ent_bytes)[pos] = b;
+        ++pos;
+      }
+    }
+  }
+}
+
+__global__ void k_cols(DevProb P, int n_cols, int n_combos, int *col_count, const int *col_off_fill) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_cols) return;
+  int c = upper_bound(P.combo_col_off, n_combos + 1, q) - 1;
+  int l = q - P.combo_col_off[c];
+  ComboRef cr = combo_ref(P, c);
+  int row0 = P.combo_row_off[c];
+  int cnt = 0, pos = col_off_fill ? col_off_fill[q] : 0;
+  for (int k = 0; k < cr.ns; ++k) {
+    int a = P.row_ent_off[row0 + k], b = P.row_ent_off[row0 + k + 1];
+    while (a < b) {  // entries of a row are sorted by l
+      int m = (a + b) >> 1;
+      if (P.ent_l[m] < l) a = m + 1; else b = m;
+    }
+    if (a < P.row_ent_off[row0 + k + 1] && P.ent_l[a] == l) {
+      if (col_off_fill) const_cast<int *>(P.col_ent)[pos++] = a;
+      else ++cnt;
+    }
+  }
+  if (!col_off_fill) col_count[q] = cnt;
+}
+
+// ---------------------------------------------------------------- simulator
+struct Scratch {
+  double *ready_f, *ready_b, *ready_g;
+  int *rem_f, *rem_b, *rem_g;
+  unsigned long long *gmask;
+};
+
+__host__ __device__ inline size_t scratch_bytes(int n_slots) {
+  size_t b = (size_t)n_slots * (3 * sizeof(double) + 3 * sizeof(int) + sizeof(unsigned long long));
+  return (b + 127) & ~(size_t)127;  // keep every warp's slice 128-byte aligned
+}
+
+__device__ inline Scratch scratch_at(char *base, int n_slots) {
+  Scratch s;
+  s.ready_f = (double *)base;
+  s.ready_b = s.ready_f + n_slots;
+  s.ready_g = s.ready_b + n_slots;
+  s.gmask = (unsigned long long *)(s.ready_g + n_slots);
+  s.rem_f = (int *)(s.gmask + n_slots);
+  s.rem_b = s.rem_f + n_slots;
+  s.rem_g = s.rem_b + n_slots;
+  return s;
+}
+
+struct WarpSmem {
+  double *qclock;
+  unsigned long long *rhi, *rlo;
+  int *raux;
+};
+
+__host__ __device__ inline size_t warp_smem_bytes(int n_queues, int cap) {
+  return (size_t)n_queues * 8 + (size_t)cap * 20 + 16;
+}
+
+__device__ inline WarpSmem warp_smem_at(char *base, int n_queues, int cap) {
+  WarpSmem w;
+  w.qclock = (double *)base;
+  w.rhi = (unsigned long long *)(w.qclock + n_queues);
+  w.rlo = w.rhi + cap;
+  w.raux = (int *)(w.rlo + cap);
+  return w;
+}
+
+struct TraceSink {
+  ps_trace_task *tasks;
+  int task_cap;
+  int *n_tasks;
+  int32_t *edge_pred;
+  unsigned long long *edge_succ;
+  int edge_cap;
+  int *n_edges;
+};
+
+struct SimOut {
+  double makespan;
+  int status;
+  int err_a, err_b;
+};
+
+__device__ __forceinline__ int group_of(const DevProb &P, int op, int g, int k) {
+  int nd = P.op_ndim[op], pm = P.op_param_mask[op];
+  int coords[PS_MAXDIM];
+  for (int i = nd - 1; i >= 0; --i) {
+    int d = P.map_deg[g * PS_MAXDIM + i];
+    coords[i] = k % d;
+    k /= d;
+  }
+  int si = 0;
+  for (int i = 0; i < nd; ++i)
+    if (pm >> i & 1) si = si * P.map_deg[g * PS_MAXDIM + i] + coords[i];
+  return si;
+}
+
+__device__ __forceinline__ int nth_bit(unsigned long long m, int n) {
+  for (int i = 0; i < n; ++i) m &= m - 1;
+  return __ffsll((long long)m) - 1;
+}
+
+// Warp-collective append to the ready set.  `n` is warp-uniform.
+__device__ __forceinline__ bool warp_push(bool want, double ready, unsigned long long key, int aux, int &n,
+                                          int cap, const WarpSmem &w, int lane) {
+  unsigned b = __ballot_sync(FULLMASK, want);
+  if (!b) return true;
+  int total = __popc(b);
+  if (n + total > cap) return false;
+  if (want) {
+    int pos = n + __popc(b & ((1u << lane) - 1u));
+    w.rhi[pos] = (unsigned long long)__double_as_longlong(ready);
+    w.rlo[pos] = key;
+    w.raux[pos] = aux;
+  }
+  n += total;
+  return true;
+}
+
+// Simulates one strategy with the calling warp.  map: [n_ops] local map
+// indices, asg: [n_slots] devices.  Exact replay of full_simulate.
+template <bool TRACE>
+__device__ SimOut warp_simulate(const DevProb &P, const int *__restrict__ map, const unsigned char *__restrict__ asg,
+                                const Scratch &S, const WarpSmem &w, int lane, const TraceSink *tr) {
+  SimOut out;
+  out.makespan = 0.0;
+  out.status = PS_STATUS_OK;
+  out.err_a = out.err_b = -1;
+  const int NF = P.n_slots;
+  for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = 0.0;
+  if (P.full)
+    for (int s = lane; s < NF; s += 32) S.gmask[s] = 0ull;
+  __syncwarp();
+  int n = 0;
+  bool okcap = true;
+  // ---- init: in-degrees, sources, ring membership
+  for (int base = 0; base < NF; base += 32) {
+    int s = base + lane;
+    bool want = false;
+    unsigned long long key = 0;
+    if (s < NF) {
+      int o = P.slot_op[s];
+      int k = s - P.op_slot_off[o];
+      int m = map[o];
+      int g = P.op_map_off[o] + m;
+      if (k < P.map_size[g]) {
+        int indeg = 0;
+        for (int i = P.op_in_off[o]; i < P.op_in_off[o + 1]; ++i) {
+          int p = P.op_in_pairs[i];
+          int sp = P.pair_src[p];
+          int nmd = P.op_map_off[o + 1] - P.op_map_off[o];
+          int c = P.combo_off[p] + map[sp] * nmd + m;
+          int col = P.combo_col_off[c] + k;
+          indeg += P.col_ent_off[col + 1] - P.col_ent_off[col];
+        }
+        S.rem_f[s] = indeg;
+        S.ready_f[s] = 0.0;
+        if (P.full) {
+          int outd = 1;
+          for (int i = P.op_out_off[o]; i < P.op_out_off[o + 1]; ++i) {
+            int p = P.op_out_pairs[i];
+            int dp = P.pair_dst[p];
+            int nmd = P.op_map_off[dp + 1] - P.op_map_off[dp];
+            int c = P.combo_off[p] + m * nmd + map[dp];
+            int row = P.combo_row_off[c] + k;
+            outd += P.row_ent_off[row + 1] - P.row_ent_off[row];
+          }
+          S.rem_b[s] = outd;
+          S.ready_b[s] = 0.0;
+          if (P.op_param_mask[o] >= 0) {
+            int si = group_of(P, o, g, k);
+            atomicOr(&S.gmask[P.op_slot_off[o] + si], 1ull << asg[s]);
+            // slot op_slot_off[o]+k doubles as the hop-0 counter of group k
+            if (k < P.map_ngroups[g]) {
+              S.rem_g[s] = P.map_size[g] / P.map_ngroups[g];
+              S.ready_g[s] = 0.0;
+            }
+          }
+        }
+        if (indeg == 0) {
+          want = true;
+          key = pack_key(KIND_OP, o, 0, k, 0);
+        }
+      }
+    }
+    okcap &= warp_push(want, 0.0, key, s, n, P.cap, w, lane);
+  }
+  __syncwarp();
+  if (!okcap) { out.status = PS_STATUS_CAPACITY; return out; }
+  int popped = 0;
+  // ---- event loop: pop the global minimum (ready, origin), as heapq does
+  while (n > 0) {
+    unsigned long long bh = ~0ull, bl = ~0ull;
+    int bp = 0;
+    for (int i = lane; i < n; i += 32) {
+      unsigned long long h = w.rhi[i], l = w.rlo[i];
+      if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; bp = i; }
+    }
+    unsigned cand = FULLMASK;
+    unsigned v, mn;
+    v = (unsigned)(bh >> 32); mn = __reduce_min_sync(FULLMASK, v); cand = __ballot_sync(FULLMASK, v == mn);
+    v = (cand >> lane & 1) ? (unsigned)bh : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+    cand &= __ballot_sync(FULLMASK, v == mn);
+    v = (cand >> lane & 1) ? (unsigned)(bl >> 32) : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+    cand &= __ballot_sync(FULLMASK, v == mn);
+    v = (cand >> lane & 1) ? (unsigned)bl : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+    cand &= __ballot_sync(FULLMASK, v == mn);
+    int win = __ffs(cand) - 1;
+    int pos = __shfl_sync(FULLMASK, bp, win);
+    unsigned long long key = w.rlo[pos];
+    double ready = __longlong_as_double((long long)w.rhi[pos]);
+    int aux = w.raux[pos];
+    __syncwarp();
+    if (lane == 0) {
+      w.rhi[pos] = w.rhi[n - 1];
+      w.rlo[pos] = w.rlo[n - 1];
+      w.raux[pos] = w.raux[n - 1];
+    }
+    --n;
+    __syncwarp();
+    // ---- decode the task: queue and exe time
+    unsigned kind = key_kind(key), a = key_a(key), b = key_b(key), c = key_c(key), d = key_d(key);
+    int q;
+    double exe, nbytes = 0.0;
+    int ring_r = 0;
+    if (kind == KIND_OP || kind == KIND_OP_BWD) {
+      int o = a;
+      int dev = asg[P.op_slot_off[o] + c];
+      q = dev;
+      int g = P.op_map_off[o] + map[o];
+      exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[g * P.n_kinds + P.dev_kind[dev]];
+    } else if (kind == KIND_SYNC) {
+      int o = a;
+      int g = P.op_map_off[o] + map[o];
+      unsigned long long msk = S.gmask[P.op_slot_off[o] + b];
+      ring_r = __popcll((long long)msk);
+      int da = nth_bit(msk, c % ring_r), db = nth_bit(msk, (c + 1) % ring_r);
+      int li = P.link_of[da * P.n_dev + db];
+      if (li < 0) { out.status = PS_STATUS_NO_ROUTE; out.err_a = da; out.err_b = db; return out; }
+      q = P.n_dev + li;
+      nbytes = P.map_shard[g] / (double)ring_r;
+      exe = P.link_lat[li] + nbytes / P.link_bw[li];
+    } else {
+      int da = asg[P.op_slot_off[a] + c], db = asg[P.op_slot_off[b] + d];
+      int li = P.link_of[da * P.n_dev + db];
+      if (li < 0) { out.status = PS_STATUS_NO_ROUTE; out.err_a = da; out.err_b = db; return out; }
+      q = P.n_dev + li;
+      long long bytes = P.ent_bytes[aux];
+      nbytes = (double)bytes;
+      exe = P.link_lat[li] + nbytes / P.link_bw[li];
+    }
+    double clk = w.qclock[q];
+    double start = ready < clk ? clk : ready;
+    double end = start + exe;
+    __syncwarp();
+    if (lane == 0) w.qclock[q] = end;
+    if (end > out.makespan) out.makespan = end;
+    int my_index = popped++;
+    if (TRACE && lane == 0) {
+      int t = atomicAdd(tr->n_tasks, 1);
+      if (t < tr->task_cap) {
+        ps_trace_task r;
+        r.key = key; r.queue = q; r.aux = aux; r.exe = exe; r.nbytes = nbytes;
+        r.ready = ready; r.start = start; r.end = end;
+        tr->tasks[t] = r;
+      }
+    }
+    // ---- relax successors
+    bool want = false;
+    unsigned long long skey = 0;
+    double sready = 0.0;
+    int saux = 0;
+#define EMIT_EDGE(succkey)                                          \
+  if (TRACE) {                                                      \
+    int e_ = atomicAdd(tr->n_edges, 1);                             \
+    if (e_ < tr->edge_cap) { tr->edge_pred[e_] = my_index; tr->edge_succ[e_] = (succkey); } \
+  }
+    if (kind == KIND_OP) {
+      int o = a, k = c, m = map[o];
+      int dev = asg[P.op_slot_off[o] + k];
+      if (P.full) {
+        int s = P.op_slot_off[o] + k;
+        want = false;
+        sready = 0.0;
+        if (lane == 0) {
+          double r = S.ready_b[s];
+          if (end > r) { r = end; S.ready_b[s] = r; }
+          EMIT_EDGE(pack_key(KIND_OP_BWD, o, 0, k, 0));
+          if (--S.rem_b[s] == 0) { want = true; sready = r; }
+        }
+        if (!warp_push(want, sready, pack_key(KIND_OP_BWD, o, 0, k, 0), s, n, P.cap, w, lane)) goto overflow;
+      }
+      for (int i = P.op_out_off[o]; i < P.op_out_off[o + 1]; ++i) {
+        int p = P.op_out_pairs[i];
+        int dp = P.pair_dst[p];
+        int nmd = P.op_map_off[dp + 1] - P.op_map_off[dp];
+        int cc = P.combo_off[p] + m * nmd + map[dp];
+        int row = P.combo_row_off[cc] + k;
+        int e0 = P.row_ent_off[row], e1 = P.row_ent_off[row + 1];
+        for (int eb = e0; eb < e1; eb += 32) {
+          int e = eb + lane;
+          want = false;
+          if (e < e1) {
+            int l = P.ent_l[e];
+            int ds = P.op_slot_off[dp] + l;
+            int ddev = asg[ds];
+            if (ddev == dev) {
+              double r = S.ready_f[ds];
+              if (end > r) { r = end; S.ready_f[ds] = r; }
+              EMIT_EDGE(pack_key(KIND_OP, dp, 0, l, 0));
+              if (--S.rem_f[ds] == 0) { want = true; sready = r; skey = pack_key(KIND_OP, dp, 0, l, 0); saux = ds; }
+            } else {
+              // link existence is checked when the transfer is dequeued
+              skey = pack_key(KIND_EDGE, o, dp, k, l);
+              EMIT_EDGE(skey);
+              want = true; sready = end; saux = e;
+            }
+          }
+          if (!warp_push(want, sready, skey, saux, n, P.cap, w, lane)) goto overflow;
+        }
+      }
+    } else if (kind == KIND_EDGE || kind == KIND_EDGE_BWD) {
+      // edge: -> op(d, l);  edge_bwd: -> op_bwd(s, k)
+      int o = kind == KIND_EDGE ? b : a;
+      int k = kind == KIND_EDGE ? d : c;
+      int s = P.op_slot_off[o] + k;
+      double *rd = kind == KIND_EDGE ? S.ready_f : S.ready_b;
+      int *rm = kind == KIND_EDGE ? S.rem_f : S.rem_b;
+      unsigned long long sk = pack_key(kind == KIND_EDGE ? KIND_OP : KIND_OP_BWD, o, 0, k, 0);
+      want = false;
+      if (lane == 0) {
+        double r = rd[s];
+        if (end > r) { r = end; rd[s] = r; }
+        EMIT_EDGE(sk);
+        if (--rm[s] == 0) { want = true; sready = r; }
+      }
+      if (!warp_push(want, sready, sk, s, n, P.cap, w, lane)) goto overflow;
+    } else if (kind == KIND_OP_BWD) {
+      int o = a, k = c, m = map[o];
+      int dev = asg[P.op_slot_off[o] + k];
+      int nmo = P.op_map_off[o + 1] - P.op_map_off[o];
+      for (int i = P.op_in_off[o]; i < P.op_in_off[o + 1]; ++i) {
+        int p = P.op_in_pairs[i];
+        int sp = P.pair_src[p];
+        int cc = P.combo_off[p] + map[sp] * nmo + m;
+        int col = P.combo_col_off[cc] + k;
+        int j0 = P.col_ent_off[col], j1 = P.col_ent_off[col + 1];
+        for (int jb = j0; jb < j1; jb += 32) {
+          int j = jb + lane;
+          want = false;
+          if (j < j1) {
+            int e = P.col_ent[j];
+            int kk = P.ent_k[e];
+            int ss = P.op_slot_off[sp] + kk;
+            int sdev = asg[ss];
+            if (sdev == dev) {
+              double r = S.ready_b[ss];
+              if (end > r) { r = end; S.ready_b[ss] = r; }
+              EMIT_EDGE(pack_key(KIND_OP_BWD, sp, 0, kk, 0));
+              if (--S.rem_b[ss] == 0) { want = true; sready = r; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); saux = ss; }
+            } else {
+              // the forward pass already proved this link exists
+              skey = pack_key(KIND_EDGE_BWD, sp, o, kk, k);
+              EMIT_EDGE(skey);
+              want = true; sready = end; saux = e;
+            }
+          }
+          if (!warp_push(want, sready, skey, saux, n, P.cap, w, lane)) goto overflow;
+        }
+      }
+      if (P.op_param_mask[o] >= 0) {
+        int g = P.op_map_off[o] + m;
+        int si = group_of(P, o, g, k);
+        int gs = P.op_slot_off[o] + si;
+        unsigned long long msk = S.gmask[gs];
+        want = false;
+        sready = 0.0;
+        if (__popcll((long long)msk) >= 2 && lane == 0) {
+          double r = S.ready_g[gs];
+          if (end > r) { r = end; S.ready_g[gs] = r; }
+          EMIT_EDGE(pack_key(KIND_SYNC, o, si, 0, 0));
+          if (--S.rem_g[gs] == 0) { want = true; sready = r; }
+        }
+        if (!warp_push(want, sready, pack_key(KIND_SYNC, o, si, 0, 0), gs, n, P.cap, w, lane)) goto overflow;
+      }
+    } else {  // KIND_SYNC: chain to the next hop of the ring
+      want = lane == 0 && (int)c + 1 < 2 * (ring_r - 1);
+      if (want) EMIT_EDGE(pack_key(KIND_SYNC, a, b, c + 1, 0));
+      if (!warp_push(want, end, pack_key(KIND_SYNC, a, b, c + 1, 0), aux, n, P.cap, w, lane)) goto overflow;
+    }
+    __syncwarp();
+  }
+#undef EMIT_EDGE
+  return out;
+overflow:
+  out.status = PS_STATUS_CAPACITY;
+  return out;
+}
+
+constexpr int WARPS_PER_BLOCK = 4;
+
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
+k_simulate_batch(DevProb P, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
+                 double *makespan, int *status, char *scratch) {
+  extern __shared__ __align__(16) char smem[];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int gw = blockIdx.x * WARPS_PER_BLOCK + wib;
+  int nw = gridDim.x * WARPS_PER_BLOCK;
+  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
+  WarpSmem w = warp_smem_at(smem + wib * wsm, P.n_queues, P.cap);
+  Scratch S = scratch_at(scratch + (size_t)gw * scratch_bytes(P.n_slots), P.n_slots);
+  for (int cand = gw; cand < n; cand += nw) {
+    SimOut o = warp_simulate<false>(P, maps + (size_t)cand * P.n_ops, asgs + (size_t)cand * P.n_slots, S, w, lane,
+                                    nullptr);
+    if (lane == 0) {
+      makespan[cand] = o.status == PS_STATUS_OK ? o.makespan : -1.0;
+      status[cand] = o.status;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(32)
+k_simulate_trace(DevProb P, const int *map, const unsigned char *asg, char *scratch, TraceSink tr,
+                 double *makespan, int *status, int *err) {
+  extern __shared__ __align__(16) char smem[];
+  int lane = threadIdx.x & 31;
+  WarpSmem w = warp_smem_at(smem, P.n_queues, P.cap);
+  Scratch S = scratch_at(scratch, P.n_slots);
+  SimOut o = warp_simulate<true>(P, map, asg, S, w, lane, &tr);
+  if (lane == 0) {
+    *makespan = o.makespan;
+    *status = o.status;
+    err[0] = o.err_a;
+    err[1] = o.err_b;
+  }
+}
+
+
+// Explicit task graph (hand-built TaskGraphs, and the oracle_simulate path):
+// one warp replays the (ready, origin-rank) heap order over CSR successors.
+// The ready set lives in global memory (capacity n_tasks).
+__global__ void __launch_bounds__(32)
+k_simulate_explicit(int n_tasks, int n_queues, const int *__restrict__ queue, const double *__restrict__ exe,
+                    const unsigned long long *__restrict__ rank, const int *__restrict__ succ_off,
+                    const int *__restrict__ succ, const int *__restrict__ indeg, double *ready, double *start,
+                    double *end, int *order, int *rem, double *qclock, unsigned long long *rhi,
+                    unsigned long long *rlo, int *raux, int *status, double *makespan) {
+  int lane = threadIdx.x;
+  for (int q = lane; q < n_queues; q += 32) qclock[q] = 0.0;
+  WarpSmem w;
+  w.qclock = qclock; w.rhi = rhi; w.rlo = rlo; w.raux = raux;
+  int n = 0;
+  for (int base = 0; base < n_tasks; base += 32) {
+    int t = base + lane;
+    bool want = false;
+    if (t < n_tasks) {
+      rem[t] = indeg[t];
+      ready[t] = 0.0;
+      want = indeg[t] == 0;
+    }
+    warp_push(want, 0.0, t < n_tasks ? rank[t] : 0ull, t, n, n_tasks, w, lane);
+  }
+  __syncwarp();
+  double mk = 0.0;
+  int popped = 0;
+  while (n > 0) {
+    unsigned long long bh = ~0ull, bl = ~0ull;
+    int bp = 0;
+    for (int i = lane; i < n; i += 32) {
+      unsigned long long h = rhi[i], l = rlo[i];
+      if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; bp = i; }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      unsigned long long oh = __shfl_xor_sync(FULLMASK, bh, off), ol = __shfl_xor_sync(FULLMASK, bl, off);
+      int op = __shfl_xor_sync(FULLMASK, bp, off);
+      if (oh < bh || (oh == bh && ol < bl)) { bh = oh; bl = ol; bp = op; }
+    }
+    int t = raux[bp];
+    double r = __longlong_as_double((long long)bh);
+    __syncwarp();
+    if (lane == 0) { rhi[bp] = rhi[n - 1]; rlo[bp] = rlo[n - 1]; raux[bp] = raux[n - 1]; }
+    --n;
+    __syncwarp();
+    int q = queue[t];
+    double clk = qclock[q];
+    double st = r < clk ? clk : r;
+    double en = st + exe[t];
+    __syncwarp();
+    if (lane == 0) { qclock[q] = en; ready[t] = r; start[t] = st; end[t] = en; order[popped] = t; }
+    ++popped;
+    if (en > mk) mk = en;
+    for (int jb = succ_off[t]; jb < succ_off[t + 1]; jb += 32) {
+      int j = jb + lane;
+      bool want = false;
+      double sr = 0.0;
+      int v = 0;
+      if (j < succ_off[t + 1]) {
+        v = succ[j];
+        sr = ready[v];
+        if (en > sr) { sr = en; ready[v] = sr; }
+        want = --rem[v] == 0;
+      }
+      warp_push(want, sr, want ? rank[v] : 0ull, v, n, n_tasks, w, lane);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    *status = popped == n_tasks ? PS_STATUS_OK : 3;
+    *makespan = mk;
+  }
+}
+
+// ---------------------------------------------------------------- MCMC
+struct ChainState {
+  double cost, best, beta, initial;
+  long long proposals, accepted;
+  unsigned long long key, ctr;  // Philox
+  int bpos, mti;                // Philox buffer position / MT index
+  int status, err_a, err_b, started;
+  int last_op, pad_;
+};
+
+__device__ __forceinline__ void philox_block(unsigned long long ctr, unsigned long long key, unsigned out[4]) {
+  unsigned c0 = (unsigned)ctr, c1 = (unsigned)(ctr >> 32), c2 = 0u, c3 = 0u;
+  unsigned k0 = (unsigned)key, k1 = (unsigned)(key >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    unsigned hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    unsigned hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    c0 = hi1 ^ c1 ^ k0; c1 = lo1; c2 = hi0 ^ c3 ^ k1; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// Warp-uniform RNG: every lane holds the same state and gets the same word.
+struct WarpRng {
+  int mode;
+  unsigned long long key, ctr;
+  unsigned buf[4];
+  int bpos;
+  unsigned *mt;  // global [624]
+  int mti;
+  int lane;
+
+  __device__ unsigned next() {
+    if (mode == PS_RNG_PHILOX) {
+      if (bpos == 4) { philox_block(ctr++, key, buf); bpos = 0; }
+      return buf[bpos++];
+    }
+    if (mti >= 624) twist();
+    unsigned y = mt[mti++];
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9d2c5680u;
+    y ^= (y << 15) & 0xefc60000u;
+    y ^= y >> 18;
+    return y;
+  }
+  // MT19937 regeneration in three dependency-free phases
+  __device__ void twist_range(int lo, int hi) {
+    for (int base = lo; base < hi; base += 32) {
+      int i = base + lane;
+      unsigned nv = 0;
+      if (i < hi) {
+        unsigned y = (mt[i] & 0x80000000u) | (mt[i + 1 < 624 ? i + 1 : 0] & 0x7fffffffu);
+        int j = i + 397 < 624 ? i + 397 : i + 397 - 624;
+        nv = mt[j] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+      }
+      __syncwarp();
+      if (i < hi) mt[i] = nv;
+      __syncwarp();
+    }
+  }
+  __device__ void twist() {
+    twist_range(0, 227);
+    twist_range(227, 454);
+    twist_range(454, 623);
+    twist_range(623, 624);
+    mti = 0;
+  }
+  __device__ unsigned below(unsigned n) {
+    int k = 32 - __clz(n);
+    unsigned v = next() >> (32 - k);
+    while (v >= n) v = next() >> (32 - k);
+    return v;
+  }
+  __device__ double random() {
+    unsigned a = next() >> 5, b = next() >> 6;
+    return ((double)a * 67108864.0 + (double)b) * (1.0 / 9007199254740992.0);
+  }
+};
+
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
+k_mcmc(DevProb P, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
+       int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
+       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *scratch) {
+  extern __shared__ __align__(16) char smem[];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int chain = blockIdx.x * WARPS_PER_BLOCK + wib;
+  if (chain >= n_chains) return;
+  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
+  char *mysm = smem + wib * (wsm + (size_t)P.n_slots * 0 + 0);
+  WarpSmem w = warp_smem_at(mysm, P.n_queues, P.cap);
+  Scratch S = scratch_at(scratch + (size_t)chain * scratch_bytes(P.n_slots), P.n_slots);
+  int *map = maps + (size_t)chain * P.n_ops;
+  unsigned char *asg = asgs + (size_t)chain * P.n_slots;
+  ChainState cs = st[chain];
+  if (cs.status != PS_STATUS_OK) return;
+  WarpRng rng;
+  rng.mode = rng_mode;
+  rng.key = cs.key;
+  rng.ctr = cs.ctr;
+  rng.bpos = cs.bpos;
+  rng.lane = lane;
+  rng.mt = mt_all ? mt_all + (size_t)chain * 624 : nullptr;
+  rng.mti = cs.mti;
+  if (rng_mode == PS_RNG_PHILOX && rng.bpos < 4) philox_block(rng.ctr - 1, rng.key, rng.buf);
+  if (!cs.started) {
+    SimOut o = warp_simulate<false>(P, map, asg, S, w, lane, nullptr);
+    cs.started = 1;
+    if (o.status != PS_STATUS_OK) {
+      cs.status = o.status; cs.err_a = o.err_a; cs.err_b = o.err_b;
+      cs.initial = cs.best = cs.cost = __longlong_as_double(0x7ff0000000000000ll);
+      if (lane == 0) st[chain] = cs;
+      return;
+    }
+    cs.cost = cs.best = cs.initial = o.makespan;
+    cs.beta = beta_given ? beta_param : (o.makespan > 0.0 ? __ddiv_rn(ln10, __dmul_rn(0.05, o.makespan)) : 1.0);
+    for (int i = lane; i < P.n_ops; i += 32) best_maps[(size_t)chain * P.n_ops + i] = map[i];
+    for (int i = lane; i < P.n_slots; i += 32) best_asgs[(size_t)chain * P.n_slots + i] = asg[i];
+  }
+  // per-warp staging for the proposal: old config of the op
+  __shared__ unsigned char old_asg_all[WARPS_PER_BLOCK][256];
+  unsigned char *old_asg = old_asg_all[wib];
+  for (int it = 0; it < proposals; ++it) {
+    // _propose_change (search.py:101-115): op, degree map, one device per task
+    int o = (int)rng.below((unsigned)P.n_ops);
+    int m = (int)rng.below((unsigned)P.op_nmaps_enum[o]);
+    cs.last_op = o;
+    int g = P.op_map_off[o] + m;
+    int size = P.map_size[g];
+    int base = P.op_slot_off[o];
+    int old_m = map[o];
+    int old_size = P.map_size[P.op_map_off[o] + old_m];
+    bool same = (m == old_m);
+    for (int i = lane; i < old_size; i += 32) old_asg[i] = asg[base + i];
+    __syncwarp();
+    for (int k = 0; k < size; ++k) {
+      unsigned dv = rng.below((unsigned)P.n_dev);
+      if (lane == 0) asg[base + k] = (unsigned char)dv;
+      same = same && (k < old_size && old_asg[k] == (unsigned char)dv);
+    }
+    if (lane == 0) map[o] = m;
+    __syncwarp();
+    double cand;
+    if (same) {
+      cand = cs.cost;
+    } else {
+      SimOut so = warp_simulate<false>(P, map, asg, S, w, lane, nullptr);
+      if (so.status != PS_STATUS_OK) {
+        cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
+        break;
+      }
+      cand = so.makespan;
+    }
+    long long idx = cs.proposals++;
+    bool ok;
+    if (cand <= cs.cost) ok = true;
+    else {
+      double p = exp(__dmul_rn(cs.beta, __dsub_rn(cs.cost, cand)));
+      ok = p >= 1.0 ? true : rng.random() < p;
+    }
+    if (trace_cap > 0 && idx < trace_cap && lane == 0) {
+      trace_cand[(size_t)chain * trace_cap + idx] = cand;
+      trace_ok[(size_t)chain * trace_cap + idx] = ok;
+    }
+    if (cand < cs.best) {
+      cs.best = cand;
+      for (int i = lane; i < P.n_ops; i += 32) best_maps[(size_t)chain * P.n_ops + i] = map[i];
+      for (int i = lane; i < P.n_slots; i += 32) best_asgs[(size_t)chain * P.n_slots + i] = asg[i];
+    }
+    if (ok) {
+      cs.cost = cand;
+      cs.accepted++;
+    } else {
+      for (int i = lane; i < old_size; i += 32) asg[base + i] = old_asg[i];
+      if (lane == 0) map[o] = old_m;
+    }
+    __syncwarp();
+  }
+  cs.key = rng.key;
+  cs.ctr = rng.ctr;
+  cs.bpos = rng.bpos;
+  cs.mti = rng.mti;
+  if (lane == 0) st[chain] = cs;
+}
+
+__global__ void k_best(const ChainState *st, int n, double *best_cost, int *best_chain) {
+  // single block argmin by (best, chain) -- earliest chain wins ties (search.py:256)
+  __shared__ double sb[1024];
+  __shared__ int si[1024];
+  double b = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = -1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = st[i].best;
+    bool live = st[i].started && st[i].initial < __longlong_as_double(0x7ff0000000000000ll);
+    if (live && (bi < 0 || v < b)) { b = v; bi = i; }
+  }
+  sb[threadIdx.x] = b;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      double ob = sb[threadIdx.x + s];
+      int oi = si[threadIdx.x + s];
+      if (oi >= 0 && (si[threadIdx.x] < 0 || ob < sb[threadIdx.x] || (ob == sb[threadIdx.x] && oi < si[threadIdx.x]))) {
+        sb[threadIdx.x] = ob;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { *best_cost = sb[0]; *best_chain = si[0]; }
+}
+
+template <class T>
+int upload(std::vector<void *> &owned, const T *host, size_t n, const T **dev) {
+  if (n == 0) { *dev = nullptr; return PS_OK; }
+  void *p = nullptr;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  CK(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  *dev = (const T *)p;
+  return PS_OK;
+}
+
+}  // namespace
+
+struct ps_problem {
+  int device;
+  DevProb P;
+  std::vector<void *> owned;
+  long long n_entries, n_combos, n_rows, n_cols;
+  size_t smem_per_block;
+  int blocks_per_sm, sm_count;
+  char *scratch = nullptr;  // batch scratch (grid-sized)
+  size_t scratch_warps = 0;
+  int *d_map = nullptr;
+  unsigned char *d_asg = nullptr;
+  double *d_mk = nullptr;
+  int *d_st = nullptr;
+  size_t io_cap = 0;
+  long long device_bytes = 0;
+};
+
+struct ps_mcmc {
+  ps_problem *prob;
+  int n;
+  ps_mcmc_params params;
+  int *maps, *best_maps;
+  unsigned char *asgs, *best_asgs;
+  ChainState *st;
+  unsigned *mt;
+  double *trace_cand;
+  unsigned char *trace_ok;
+  char *scratch;
+  double *d_best;
+  int *d_bestc;
+};
+
+static int ensure_io(ps_problem *pr, size_t n) {
+  if (n <= pr->io_cap) return PS_OK;
+  cudaFree(pr->d_map); cudaFree(pr->d_asg); cudaFree(pr->d_mk); cudaFree(pr->d_st);
+  CK(cudaMalloc(&pr->d_map, n * pr->P.n_ops * sizeof(int)));
+  CK(cudaMalloc(&pr->d_asg, n * (size_t)pr->P.n_slots));
+  CK(cudaMalloc(&pr->d_mk, n * sizeof(double)));
+  CK(cudaMalloc(&pr->d_st, n * sizeof(int)));
+  pr->io_cap = n;
+  return PS_OK;
+}
+
+extern "C" {
+
+const char *ps_last_error(void) { return g_err.c_str(); }
+int ps_abi_version(void) { return PS_ABI_VERSION; }
+
+int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
+  if (!d || !out) return fail(PS_ERR_INVALID, "null argument");
+  if (d->abi_version != PS_ABI_VERSION) return fail(PS_ERR_INVALID, "ABI version mismatch");
+  if (d->n_devices > 64) return fail(PS_ERR_INVALID, "at most 64 devices per topology are supported");
+  if (d->n_ops >= 65536) return fail(PS_ERR_INVALID, "at most 65535 operations are supported");
+  CK(cudaSetDevice(device));
+  ps_problem *pr = new ps_problem();
+  pr->device = device;
+  DevProb &P = pr->P;
+  P.n_ops = d->n_ops; P.n_dev = d->n_devices; P.n_kinds = d->n_kinds; P.n_links = d->n_links;
+  P.n_pairs = d->n_pairs; P.n_maps = d->n_maps; P.full = d->mode_full; P.n_slots = d->n_slots;
+  P.n_queues = d->n_devices + d->n_links;
+  P.cap = d->ready_capacity > 0 ? d->ready_capacity : 256;
+  std::vector<void *> &ow = pr->owned;
+  int n_combos = 0;
+  n_combos = d->combo_off[d->n_pairs];
+  int n_rows = d->combo_row_off[n_combos], n_cols = d->combo_col_off[n_combos];
+  int n_need = d->pair_need_off[d->n_pairs];
+  int rc = PS_OK;
+#define UP(field, count) \
+  if ((rc = upload(ow, d->field, (size_t)(count), &P.field)) != PS_OK) { ps_problem_destroy(pr); return rc; }
+  UP(dev_kind, P.n_dev);
+  UP(link_of, (size_t)P.n_dev * P.n_dev);
+  UP(link_bw, P.n_links);
+  UP(link_lat, P.n_links);
+  UP(op_ndim, P.n_ops);
+  if ((rc = upload(ow, (const long long *)d->op_dim, (size_t)P.n_ops * PS_MAXDIM, &P.op_dim)) != PS_OK) {
+    ps_problem_destroy(pr); return rc;
+  }
+  UP(op_esize, P.n_ops);
+  UP(op_param_mask, P.n_ops);
+  UP(op_map_off, P.n_ops + 1);
+  UP(op_nmaps_enum, P.n_ops);
+  UP(op_slot_off, P.n_ops + 1);
+  UP(slot_op, P.n_slots);
+  UP(op_in_off, P.n_ops + 1);
+  UP(op_in_pairs, d->op_in_off[P.n_ops]);
+  UP(op_out_off, P.n_ops + 1);
+  UP(op_out_pairs, d->op_out_off[P.n_ops]);
+  UP(map_deg, (size_t)P.n_maps * PS_MAXDIM);
+  UP(map_size, P.n_maps);
+  UP(exe_fwd, (size_t)P.n_maps * P.n_kinds);
+  UP(exe_bwd, (size_t)P.n_maps * P.n_kinds);
+  UP(map_shard, P.n_maps);
+  UP(map_ngroups, P.n_maps);
+  UP(pair_src, P.n_pairs);
+  UP(pair_dst, P.n_pairs);
+  UP(pair_need_off, P.n_pairs + 1);
+  UP(need, (size_t)n_need * PS_MAXDIM * PS_NEED_STRIDE);
+  UP(combo_off, P.n_pairs + 1);
+  UP(combo_row_off, n_combos + 1);
+  UP(combo_col_off, n_combos + 1);
+#undef UP
+  pr->n_combos = n_combos; pr->n_rows = n_rows; pr->n_cols = n_cols;
+  // ---- overlap tables: count rows -> scan -> fill, then the column index
+  int *cnt = nullptr, *off = nullptr, *ccnt = nullptr, *coff = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0, t2 = 0;
+  CK(cudaMalloc(&cnt, (n_rows + 1) * sizeof(int)));
+  CK(cudaMalloc(&off, (n_rows + 1) * sizeof(int)));
+  CK(cudaMalloc(&ccnt, (n_cols + 1) * sizeof(int)));
+  CK(cudaMalloc(&coff, (n_cols + 1) * sizeof(int)));
+  ow.push_back(off); ow.push_back(coff);
+  CK(cudaMemset(cnt, 0, (n_rows + 1) * sizeof(int)));
+  CK(cudaMemset(ccnt, 0, (n_cols + 1) * sizeof(int)));
+  if (n_rows) k_rows<<<(n_rows + 127) / 128, 128>>>(P, n_rows, n_combos, cnt, nullptr);
+  CK(cudaGetLastError());
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, n_rows + 1);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, ccnt, coff, n_cols + 1);
+  tmp_bytes = std::max(tmp_bytes, t2);
+  CK(cudaMalloc(&tmp, tmp_bytes));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, n_rows + 1));
+  int n_ent = 0;
+  CK(cudaMemcpy(&n_ent, off + n_rows, sizeof(int), cudaMemcpyDeviceToHost));
+  pr->n_entries = n_ent;
+  unsigned short *ek = nullptr, *el = nullptr;
+  long long *eb = nullptr;
+  int *cent = nullptr;
+  CK(cudaMalloc(&ek, (n_ent + 1) * sizeof(unsigned short)));
+  CK(cudaMalloc(&el, (n_ent + 1) * sizeof(unsigned short)));
+  CK(cudaMalloc(&eb, (n_ent + 1) * sizeof(long long)));
+  CK(cudaMalloc(&cent, (n_ent + 1) * sizeof(int)));
+  ow.push_back(ek); ow.push_back(el); ow.push_back(eb); ow.push_back(cent);
+  P.ent_k = ek; P.ent_l = el; P.ent_bytes = eb; P.col_ent = cent; P.row_ent_off = off;
+  if (n_rows) k_rows<<<(n_rows + 127) / 128, 128>>>(P, n_rows, n_combos, nullptr, off);
+  CK(cudaGetLastError());
+  if (n_cols) k_cols<<<(n_cols + 127) / 128, 128>>>(P, n_cols, n_combos, ccnt, nullptr);
+  CK(cudaGetLastError());
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, ccnt, coff, n_cols + 1));
+  P.col_ent_off = coff;
+  if (n_cols) k_cols<<<(n_cols + 127) / 128, 128>>>(P, n_cols, n_combos, nullptr, coff);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  cudaFree(cnt); cudaFree(ccnt); cudaFree(tmp);
+  // ---- launch geometry for the warp-per-candidate kernels
+  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
+  pr->smem_per_block = wsm * WARPS_PER_BLOCK;
+  if (pr->smem_per_block > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
+    CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
+  }
+  if (wsm > 48 * 1024) CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+  CK(cudaDeviceGetAttribute(&pr->sm_count, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pr->blocks_per_sm, k_simulate_batch, WARPS_PER_BLOCK * 32,
+                                                   pr->smem_per_block));
+  if (pr->blocks_per_sm < 1) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "per-warp shared memory too large"); }
+  pr->device_bytes = 0;
+  *out = pr;
+  return PS_OK;
+}
+
+void ps_problem_destroy(ps_problem *pr) {
+  if (!pr) return;
+  cudaSetDevice(pr->device);
+  for (void *p : pr->owned) cudaFree(p);
+  cudaFree(pr->scratch);
+  cudaFree(pr->d_map); cudaFree(pr->d_asg); cudaFree(pr->d_mk); cudaFree(pr->d_st);
+  delete pr;
+}
+
+int ps_problem_info_get(const ps_problem *pr, ps_problem_info *o) {
+  if (!pr || !o) return fail(PS_ERR_INVALID, "null argument");
+  o->n_entries = pr->n_entries;
+  o->n_combos = pr->n_combos;
+  o->n_queues = pr->P.n_queues;
+  o->n_slots = pr->P.n_slots;
+  o->ready_capacity = pr->P.cap;
+  o->warps_per_block = WARPS_PER_BLOCK;
+  o->device_bytes = pr->device_bytes;
+  return PS_OK;
+}
+
+int ps_combo_entries(ps_problem *pr, int pair, int src_map, int dst_map, int cap, int32_t *k_out,
+                     int32_t *l_out, int64_t *bytes_out, int *n_out) {
+  CK(cudaSetDevice(pr->device));
+  // host copies of the small offset tables are not kept; fetch what we need
+  int co[2];
+  CK(cudaMemcpy(co, pr->P.combo_off + pair, sizeof(int), cudaMemcpyDeviceToHost));
+  int dst = 0, md[2];
+  CK(cudaMemcpy(&dst, pr->P.pair_dst + pair, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(md, pr->P.op_map_off + dst, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  int c = co[0] + src_map * (md[1] - md[0]) + dst_map;
+  int ro[2];
+  CK(cudaMemcpy(ro, pr->P.combo_row_off + c, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  int e[2];
+  CK(cudaMemcpy(&e[0], pr->P.row_ent_off + ro[0], sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&e[1], pr->P.row_ent_off + ro[1], sizeof(int), cudaMemcpyDeviceToHost));
+  int n = e[1] - e[0];
+  *n_out = n;
+  if (n > cap) return fail(PS_ERR_INVALID, "buffer too small");
+  std::vector<unsigned short> k(n), l(n);
+  std::vector<long long> b(n);
+  if (n) {
+    CK(cudaMemcpy(k.data(), pr->P.ent_k + e[0], n * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(l.data(), pr->P.ent_l + e[0], n * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), pr->P.ent_bytes + e[0], n * 8, cudaMemcpyDeviceToHost));
+  }
+  for (int i = 0; i < n; ++i) { k_out[i] = k[i]; l_out[i] = l[i]; bytes_out[i] = b[i]; }
+  return PS_OK;
+}
+
+int ps_simulate_batch(ps_problem *pr, const int32_t *map_local, const uint8_t *assign, int n, double *makespan_out,
+                      int32_t *status_out, int flags, void *stream) {
+  if (!pr || n < 0) return fail(PS_ERR_INVALID, "bad arguments");
+  if (n == 0) return PS_OK;
+  CK(cudaSetDevice(pr->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int *dm = map_local;
+  const unsigned char *da = assign;
+  double *dk = makespan_out;
+  int *ds = status_out;
+  if (flags != PS_DEVICE_PTRS) {
+    int rc = ensure_io(pr, n);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(pr->d_map, map_local, (size_t)n * pr->P.n_ops * sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(pr->d_asg, assign, (size_t)n * pr->P.n_slots, cudaMemcpyHostToDevice, s));
+    dm = pr->d_map; da = pr->d_asg; dk = pr->d_mk; ds = pr->d_st;
+  }
+  int blocks = std::min((n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, pr->sm_count * pr->blocks_per_sm);
+  size_t warps = (size_t)blocks * WARPS_PER_BLOCK;
+  if (warps > pr->scratch_warps) {
+    cudaFree(pr->scratch);
+    size_t want = (size_t)pr->sm_count * pr->blocks_per_sm * WARPS_PER_BLOCK;
+    CK(cudaMalloc(&pr->scratch, want * scratch_bytes(pr->P.n_slots)));
+    pr->scratch_warps = want;
+  }
+  k_simulate_batch<<<blocks, WARPS_PER_BLOCK * 32, pr->smem_per_block, s>>>(pr->P, dm, da, n, dk, ds, pr->scratch);
+  CK(cudaGetLastError());
+  if (flags != PS_DEVICE_PTRS) {
+    CK(cudaMemcpyAsync(makespan_out, dk, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(status_out, ds, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return PS_OK;
+}
+
+int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *assign, int task_cap,
+                      ps_trace_task *tasks, int *n_tasks, int edge_cap, int32_t *edge_pred, uint64_t *edge_succ_key,
+                      int *n_edges, double *makespan, int32_t *status, int32_t *err_devices) {
+  CK(cudaSetDevice(pr->device));
+  int rc = ensure_io(pr, 1);
+  if (rc) return rc;
+  char *scr = nullptr;
+  ps_trace_task *dt = nullptr;
+  int32_t *dep = nullptr;
+  unsigned long long *des = nullptr;
+  int *cnts = nullptr, *err = nullptr;
+  double *dmk = nullptr;
+  CK(cudaMalloc(&scr, scratch_bytes(pr->P.n_slots)));
+  CK(cudaMalloc(&dt, sizeof(ps_trace_task) * (size_t)std::max(task_cap, 1)));
+  CK(cudaMalloc(&dep, sizeof(int32_t) * (size_t)std::max(edge_cap, 1)));
+  CK(cudaMalloc(&des, sizeof(unsigned long long) * (size_t)std::max(edge_cap, 1)));
+  CK(cudaMalloc(&cnts, 2 * sizeof(int)));
+  CK(cudaMalloc(&err, 3 * sizeof(int)));
+  CK(cudaMalloc(&dmk, sizeof(double)));
+  CK(cudaMemset(cnts, 0, 2 * sizeof(int)));
+  CK(cudaMemcpy(pr->d_map, map_local, pr->P.n_ops * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(pr->d_asg, assign, pr->P.n_slots, cudaMemcpyHostToDevice));
+  TraceSink tr;
+  tr.tasks = dt; tr.task_cap = task_cap; tr.n_tasks = cnts; tr.edge_pred = dep; tr.edge_succ = des;
+  tr.edge_cap = edge_cap; tr.n_edges = cnts + 1;
+  size_t wsm = (warp_smem_bytes(pr->P.n_queues, pr->P.cap) + 15) & ~(size_t)15;
+  k_simulate_trace<<<1, 32, wsm>>>(pr->P, pr->d_map, pr->d_asg, scr, tr, dmk, err + 2, err);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  int h[2], he[3];
+  CK(cudaMemcpy(h, cnts, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(he, err, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(makespan, dmk, sizeof(double), cudaMemcpyDeviceToHost));
+  *n_tasks = h[0];
+  *n_edges = h[1];
+  *status = he[2];
+  err_devices[0] = he[0];
+  err_devices[1] = he[1];
+  if (h[0] <= task_cap && h[0] > 0) CK(cudaMemcpy(tasks, dt, sizeof(ps_trace_task) * h[0], cudaMemcpyDeviceToHost));
+  if (h[1] <= edge_cap && h[1] > 0) {
+    CK(cudaMemcpy(edge_pred, dep, sizeof(int32_t) * h[1], cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(edge_succ_key, des, sizeof(uint64_t) * h[1], cudaMemcpyDeviceToHost));
+  }
+  cudaFree(scr); cudaFree(dt); cudaFree(dep); cudaFree(des); cudaFree(cnts); cudaFree(err); cudaFree(dmk);
+  if (h[0] > task_cap || h[1] > edge_cap) return fail(PS_ERR_CAPACITY, "trace buffers too small");
+  return PS_OK;
+}
+
+
+int ps_simulate_explicit(int n_tasks, int n_queues, const int32_t *queue, const double *exe, const uint64_t *rank,
+                         const int32_t *succ_off, const int32_t *succ, double *ready, double *start, double *end,
+                         int32_t *order, double *makespan, int32_t *status, int device) {
+  if (n_tasks < 0 || n_queues < 0) return fail(PS_ERR_INVALID, "bad arguments");
+  CK(cudaSetDevice(device));
+  int n = n_tasks > 0 ? n_tasks : 1, nq = n_queues > 0 ? n_queues : 1;
+  int n_edges = n_tasks > 0 ? succ_off[n_tasks] : 0;
+  std::vector<int> indeg(n, 0);
+  for (int e = 0; e < n_edges; ++e) {
+    if (succ[e] < 0 || succ[e] >= n_tasks) return fail(PS_ERR_INVALID, "successor out of range");
+    indeg[succ[e]]++;
+  }
+  for (int t = 0; t < n_tasks; ++t)
+    if (queue[t] < 0 || queue[t] >= n_queues) return fail(PS_ERR_INVALID, "queue out of range");
+  std::vector<void *> tmp;
+  auto alloc = [&](size_t bytes) -> void * { void *p = nullptr; if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr; tmp.push_back(p); return p; };
+  int *dq = (int *)alloc(n * 4), *dso = (int *)alloc((n + 1) * 4), *ds = (int *)alloc((n_edges + 1) * 4);
+  int *dind = (int *)alloc(n * 4), *drem = (int *)alloc(n * 4), *dord = (int *)alloc(n * 4), *draux = (int *)alloc(n * 4);
+  double *dexe = (double *)alloc(n * 8), *drd = (double *)alloc(n * 8), *dst = (double *)alloc(n * 8),
+         *den = (double *)alloc(n * 8), *dqc = (double *)alloc(nq * 8), *dmk = (double *)alloc(8);
+  unsigned long long *drank = (unsigned long long *)alloc(n * 8), *drhi = (unsigned long long *)alloc(n * 8),
+                     *drlo = (unsigned long long *)alloc(n * 8);
+  int *dstat = (int *)alloc(4);
+  for (void *p : tmp) if (!p) { for (void *q : tmp) cudaFree(q); return fail(PS_ERR_CUDA, "cudaMalloc failed"); }
+  int rc = PS_OK;
+  do {
+    if (n_tasks) {
+      if (cudaMemcpy(dq, queue, n_tasks * 4, cudaMemcpyHostToDevice) ||
+          cudaMemcpy(dso, succ_off, (n_tasks + 1) * 4, cudaMemcpyHostToDevice) ||
+          (n_edges && cudaMemcpy(ds, succ, n_edges * 4, cudaMemcpyHostToDevice)) ||
+          cudaMemcpy(dind, indeg.data(), n_tasks * 4, cudaMemcpyHostToDevice) ||
+          cudaMemcpy(dexe, exe, n_tasks * 8, cudaMemcpyHostToDevice) ||
+          cudaMemcpy(drank, rank, n_tasks * 8, cudaMemcpyHostToDevice)) { rc = fail(PS_ERR_CUDA, "copy failed"); break; }
+    }
+    k_simulate_explicit<<<1, 32>>>(n_tasks, nq, dq, dexe, drank, dso, ds, dind, drd, dst, den, dord, drem, dqc, drhi,
+                                   drlo, draux, dstat, dmk);
+    if (cudaDeviceSynchronize() != cudaSuccess) { rc = fail(PS_ERR_CUDA, cudaGetErrorString(cudaGetLastError())); break; }
+    if (n_tasks && (cudaMemcpy(ready, drd, n_tasks * 8, cudaMemcpyDeviceToHost) ||
+                    cudaMemcpy(start, dst, n_tasks * 8, cudaMemcpyDeviceToHost) ||
+                    cudaMemcpy(end, den, n_tasks * 8, cudaMemcpyDeviceToHost) ||
+                    cudaMemcpy(order, dord, n_tasks * 4, cudaMemcpyDeviceToHost))) { rc = fail(PS_ERR_CUDA, "copy back failed"); break; }
+    cudaMemcpy(makespan, dmk, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(status, dstat, 4, cudaMemcpyDeviceToHost);
+  } while (0);
+  for (void *p : tmp) cudaFree(p);
+  return rc;
+}
+
+int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const int32_t *init_map,
+                   const uint8_t *init_assign, const uint64_t *seeds, const uint32_t *mt_state, ps_mcmc **out) {
+  if (!pr || !params || n <= 0 || !out) return fail(PS_ERR_INVALID, "bad arguments");
+  if (params->rng_mode == PS_RNG_MT19937 && !mt_state) return fail(PS_ERR_INVALID, "MT19937 mode needs mt_state");
+  CK(cudaSetDevice(pr->device));
+  ps_mcmc *m = new ps_mcmc();
+  memset(m, 0, sizeof(*m));
+  m->prob = pr;
+  m->n = n;
+  m->params = *params;
+  const DevProb &P = pr->P;
+  CK(cudaMalloc(&m->maps, (size_t)n * P.n_ops * sizeof(int)));
+  CK(cudaMalloc(&m->best_maps, (size_t)n * P.n_ops * sizeof(int)));
+  CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
+  CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
+  CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
+  CK(cudaMalloc(&m->scratch, (size_t)n * scratch_bytes(P.n_slots)));
+  CK(cudaMalloc(&m->d_best, sizeof(double)));
+  CK(cudaMalloc(&m->d_bestc, sizeof(int)));
+  CK(cudaMemcpy(m->maps, init_map, (size_t)n * P.n_ops * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m->asgs, init_assign, (size_t)n * P.n_slots, cudaMemcpyHostToDevice));
+  std::vector<ChainState> st(n);
+  for (int i = 0; i < n; ++i) {
+    ChainState &c = st[i];
+    memset(&c, 0, sizeof c);
+    c.key = seeds[i];
+    c.ctr = 0;
+    c.bpos = 4;
+    c.mti = params->rng_mode == PS_RNG_MT19937 ? (int)mt_state[(size_t)i * 625 + 624] : 624;
+  }
+  CK(cudaMemcpy(m->st, st.data(), (size_t)n * sizeof(ChainState), cudaMemcpyHostToDevice));
+  if (params->rng_mode == PS_RNG_MT19937) {
+    std::vector<unsigned> words((size_t)n * 624);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < 624; ++j) words[(size_t)i * 624 + j] = mt_state[(size_t)i * 625 + j];
+    CK(cudaMalloc(&m->mt, words.size() * sizeof(unsigned)));
+    CK(cudaMemcpy(m->mt, words.data(), words.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+  }
+  if (params->record_trace && params->trace_capacity > 0) {
+    CK(cudaMalloc(&m->trace_cand, (size_t)n * params->trace_capacity * sizeof(double)));
+    CK(cudaMalloc(&m->trace_ok, (size_t)n * params->trace_capacity));
+  }
+  *out = m;
+  return PS_OK;
+}
+
+int ps_mcmc_run(ps_mcmc *m, int proposals, void *stream) {
+  if (!m || proposals < 0) return fail(PS_ERR_INVALID, "bad arguments");
+  ps_problem *pr = m->prob;
+  CK(cudaSetDevice(pr->device));
+  int blocks = (m->n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+  size_t smem = pr->smem_per_block;
+  k_mcmc<<<blocks, WARPS_PER_BLOCK * 32, smem, (cudaStream_t)stream>>>(
+      pr->P, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
+      m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
+      m->params.record_trace ? m->params.trace_capacity : 0, m->scratch);
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_mcmc_read(ps_mcmc *m, ps_chain_summary *summary, int32_t *best_map, uint8_t *best_assign, double *trace_cand,
+                 uint8_t *trace_ok) {
+  ps_problem *pr = m->prob;
+  CK(cudaSetDevice(pr->device));
+  CK(cudaDeviceSynchronize());
+  std::vector<ChainState> st(m->n);
+  CK(cudaMemcpy(st.data(), m->st, (size_t)m->n * sizeof(ChainState), cudaMemcpyDeviceToHost));
+  if (summary) {
+    for (int i = 0; i < m->n; ++i) {
+      ps_chain_summary &s = summary[i];
+      s.initial_cost = st[i].initial; s.best_cost = st[i].best; s.cost = st[i].cost; s.beta = st[i].beta;
+      s.proposals = st[i].proposals; s.accepted = st[i].accepted; s.status = st[i].status;
+      s.err_a = st[i].err_a; s.err_b = st[i].err_b; s.last_op = st[i].last_op;
+    }
+  }
+  if (best_map) CK(cudaMemcpy(best_map, m->best_maps, (size_t)m->n * pr->P.n_ops * sizeof(int), cudaMemcpyDeviceToHost));
+  if (best_assign) CK(cudaMemcpy(best_assign, m->best_asgs, (size_t)m->n * pr->P.n_slots, cudaMemcpyDeviceToHost));
+  size_t tc = (size_t)m->n * m->params.trace_capacity;
+  if (trace_cand && m->trace_cand) CK(cudaMemcpy(trace_cand, m->trace_cand, tc * sizeof(double), cudaMemcpyDeviceToHost));
+  if (trace_ok && m->trace_ok) CK(cudaMemcpy(trace_ok, m->trace_ok, tc, cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+
+int ps_mcmc_stop(ps_mcmc *m, const uint8_t *stop) {
+  if (!m || !stop) return fail(PS_ERR_INVALID, "bad arguments");
+  CK(cudaSetDevice(m->prob->device));
+  CK(cudaDeviceSynchronize());
+  std::vector<ChainState> st(m->n);
+  CK(cudaMemcpy(st.data(), m->st, (size_t)m->n * sizeof(ChainState), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < m->n; ++i)
+    if (stop[i] && st[i].status == PS_STATUS_OK) st[i].status = PS_STATUS_STOPPED;
+  CK(cudaMemcpy(m->st, st.data(), (size_t)m->n * sizeof(ChainState), cudaMemcpyHostToDevice));
+  return PS_OK;
+}
+
+
+int ps_mcmc_chains(const ps_mcmc *m) { return m ? m->n : 0; }
+
+int ps_mcmc_read_state(ps_mcmc *m, int32_t *maps, uint8_t *assign) {
+  if (!m) return fail(PS_ERR_INVALID, "bad arguments");
+  ps_problem *pr = m->prob;
+  CK(cudaSetDevice(pr->device));
+  CK(cudaDeviceSynchronize());
+  if (maps) CK(cudaMemcpy(maps, m->maps, (size_t)m->n * pr->P.n_ops * sizeof(int), cudaMemcpyDeviceToHost));
+  if (assign) CK(cudaMemcpy(assign, m->asgs, (size_t)m->n * pr->P.n_slots, cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+int ps_mcmc_best(ps_mcmc *m, double *best_cost, int32_t *best_chain) {
+  CK(cudaSetDevice(m->prob->device));
+  k_best<<<1, 1024>>>(m->st, m->n, m->d_best, m->d_bestc);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(best_cost, m->d_best, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(best_chain, m->d_bestc, sizeof(int), cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+void ps_mcmc_destroy(ps_mcmc *m) {
+  if (!m) return;
+  cudaSetDevice(m->prob->device);
+  cudaFree(m->maps); cudaFree(m->best_maps); cudaFree(m->asgs); cudaFree(m->best_asgs); cudaFree(m->st);
+  cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok); cudaFree(m->scratch);
+  cudaFree(m->d_best); cudaFree(m->d_bestc);
+  delete m;
+}
+
+}  // extern "C"

@@ -1,0 +1,470 @@
+"""Strategy search: the reference's ``parasim.search`` API on the GPU path.
+
+``mcmc_search`` runs every chain at once, one warp per chain (``k_mcmc``),
+instead of one after another (reference search.py:193): chain c keeps the
+reference's own seed ``params.seed + 1000003*c`` and, by default, CPython's
+MT19937 stream for it, so each chain replays the unmodified reference's
+proposals, accept/reject decisions, trace and best strategy
+(``rng="philox"`` selects the shared counter-based stream of :mod:`.rng`).
+A rejected proposal costs nothing to roll back: the chain's fragment (one
+degree-map index and that op's devices) is restored in place.
+
+The polish step and the local-optimality probe scan single-op neighbours in
+the reference's enumeration order, evaluated in GPU batches, and keep the
+reference's first-improvement semantics exactly (search.py:130-167,408-438).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+import math
+import random
+import time
+from dataclasses import dataclass, field
+from itertools import islice, product
+
+import numpy as np
+
+from . import _native as nat
+from .cost import CostProfile
+from .graph import DeviceTopology, OperatorGraph
+from .lowering import MODE_FORWARD, degree_tuple, lower
+from .partition import (ParallelizationConfig, ParallelizationStrategy, data_parallel_strategy,
+                        enumerate_configs, output_region, random_strategy)
+from .rng import RNG_MT19937, RNG_PHILOX, mt_state_words
+
+__all__ = [
+    "SearchParams", "SearchReport", "ChainSummary", "SearchError", "SearchSpaceTooLarge",
+    "ExhaustiveResult", "accept_probability", "accept", "propose", "mcmc_search",
+    "exhaustive_optimal", "local_optimality_check", "evaluate_strategies",
+]
+
+_logger = logging.getLogger(__name__)
+
+
+class SearchError(RuntimeError):
+    pass
+
+
+class SearchSpaceTooLarge(RuntimeError):
+    pass
+
+
+@dataclass
+class SearchParams:
+    budget_seconds: float | None = None
+    max_proposals: int | None = None
+    beta: float | None = None
+    max_degree: int = 4
+    seed: int = 0
+    initial: list | None = None
+    mode: str = MODE_FORWARD
+    stagnation_floor: float = 2.0
+    check_interval: int = 0
+    polish: bool = True
+    polish_cap: float = 2e5
+    # B200 path knobs (new, optional)
+    rng: str = RNG_MT19937          # "mt19937" replays the reference; "philox" = shared Philox stream
+    segment: int = 256              # proposals per kernel launch between host checks
+    device: int = 0
+
+
+@dataclass
+class ChainSummary:
+    index: int
+    initial_cost: float
+    best_cost: float
+    proposals: int
+    accepted: int
+    beta: float
+    termination: str
+
+
+@dataclass
+class SearchReport:
+    best_strategy: ParallelizationStrategy
+    best_cost: float
+    trace: list = field(default_factory=list)
+    proposals: int = 0
+    termination: str = "budget"
+    chains: list = field(default_factory=list)
+
+
+def accept_probability(cost_s: float, cost_s_star: float, beta: float) -> float:
+    """min(1, exp(beta * (cost_s - cost_s_star))) (reference search.py:89-93)."""
+    return 1.0 if cost_s_star <= cost_s else math.exp(beta * (cost_s - cost_s_star))
+
+
+def accept(cost_s: float, cost_s_star: float, beta: float, rng: random.Random) -> bool:
+    """Draws rng.random() only when the move is uphill (search.py:96-98)."""
+    p = accept_probability(cost_s, cost_s_star, beta)
+    return p >= 1.0 or rng.random() < p
+
+
+def _propose_change(strategy, g, topo, max_degree, rng, config_cache):
+    """Uniform op, uniform degree map, uniform device per task (search.py:101-115)."""
+    op_id = rng.choice(sorted(g.ops))
+    choices = config_cache.get(op_id)
+    if choices is None:
+        choices = config_cache[op_id] = enumerate_configs(g.ops[op_id], topo, max_degree)
+    picked = rng.choice(choices)
+    devices = topo.device_ids()
+    return op_id, ParallelizationConfig(dict(picked.degrees),
+                                        tuple(rng.choice(devices) for _ in range(picked.size())))
+
+
+def propose(strategy: ParallelizationStrategy, g: OperatorGraph, topo: DeviceTopology, max_degree: int,
+            rng: random.Random) -> ParallelizationStrategy:
+    op_id, cfg = _propose_change(strategy, g, topo, max_degree, rng, {})
+    out = strategy.copy()
+    out.configs[op_id] = cfg
+    return out
+
+
+# -----------------------------------------------------------------------------
+# batched evaluation
+
+def evaluate_strategies(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile, strategies,
+                        mode: str = MODE_FORWARD, max_degree: int | None = None, low=None) -> np.ndarray:
+    """Makespans of many strategies in one GPU launch (ps_simulate_batch).
+    Raises like build_task_graph for the first failing strategy."""
+    from .taskgraph import TaskGraph, _bind, _check_config, _raise_status
+    strategies = list(strategies)
+    for s in strategies:
+        for oid in sorted(g.ops):
+            _check_config(g, topo, oid, s.configs[oid])
+    if low is None or not all(low.has_maps_for(s) for s in strategies):
+        low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=strategies)
+    n = len(strategies)
+    maps = np.zeros((n, low.n_ops), dtype=np.int32)
+    asg = np.zeros((n, low.n_slots), dtype=np.uint8)
+    for i, s in enumerate(strategies):
+        low.encode(s, maps[i], asg[i])
+    return _eval_encoded(low, maps, asg, strategies)
+
+
+def _eval_encoded(low, maps, asg, strategies=None):
+    from .taskgraph import TaskGraph, _bind, _raise_status
+    n = maps.shape[0]
+    mk = np.zeros(n, dtype=np.float64)
+    st = np.zeros(n, dtype=np.int32)
+    nat.check(nat.lib().ps_simulate_batch(low.handle(), nat.ptr(maps), nat.ptr(asg), n, nat.ptr(mk), nat.ptr(st),
+                                          nat.PS_HOST_PTRS, None), "ps_simulate_batch")
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        i = int(bad[0])
+        strat = strategies[i] if strategies is not None else low.decode(maps[i], asg[i])
+        tg = TaskGraph(low.graph, low.topology, strat, low.profile, low.mode)
+        _bind(tg, low)
+        _raise_status(tg, int(st[i]))
+    return mk
+
+
+# -----------------------------------------------------------------------------
+# MCMC
+
+def _chain_error_text(exc: Exception) -> str:
+    return f"error: {exc}"
+
+
+def mcmc_search(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile,
+                params: SearchParams) -> SearchReport:
+    """Metropolis-Hastings over single-op config changes, one GPU warp per
+    chain (reference search.py:170-271)."""
+    from .taskgraph import NoRouteError, TaskGraph, _bind, _check_config, _first_missing_route
+    if params.budget_seconds is None and params.max_proposals is None:
+        raise ValueError("SearchParams needs budget_seconds or max_proposals")
+    initial = params.initial
+    if initial is None:
+        initial = [data_parallel_strategy(g, topo), random_strategy(g, topo, params.max_degree, params.seed)]
+    g.topological_order()
+    n = len(initial)
+    start_err: dict[int, str] = {}
+    live = []
+    for ci, s0 in enumerate(initial):
+        try:
+            for oid in sorted(g.ops):
+                if oid not in s0.configs:
+                    raise KeyError(oid)
+                _check_config(g, topo, oid, s0.configs[oid])
+            live.append(ci)
+        except Exception as exc:  # noqa: BLE001 - same isolation as the reference
+            start_err[ci] = _chain_error_text(exc)
+    summaries: list[ChainSummary | None] = [None] * n
+    traces: list[list] = [[] for _ in range(n)]
+    best: dict[int, tuple[float, ParallelizationStrategy]] = {}
+    if live:
+        low = lower(g, topo, profile, params.mode, max_degree=params.max_degree,
+                    strategies=[initial[c] for c in live], device=params.device)
+        _run_chains(low, params, initial, live, summaries, traces, best, start_err)
+    for ci, msg in start_err.items():
+        if summaries[ci] is None:
+            _logger.warning("chain %d failed to start: %s", ci, msg[len("error: "):])
+            summaries[ci] = ChainSummary(ci, math.inf, math.inf, 0, 0, 0.0, msg)
+    trace: list = []
+    iteration = 0
+    best_overall = None
+    for ci in range(n):
+        for cand, ok in traces[ci]:
+            iteration += 1
+            trace.append((iteration, cand, ok))
+        if ci in best and (best_overall is None or best[ci][0] < best_overall[0]):
+            best_overall = (best[ci][0], best[ci][1], ci, summaries[ci].termination)
+    if best_overall is None:
+        raise SearchError("every chain failed")
+    best_cost, best_strategy, _, termination = best_overall
+    if params.polish:
+        best_cost, best_strategy = _greedy_descend(g, topo, profile, best_strategy, best_cost, params)
+    return SearchReport(best_strategy=best_strategy, best_cost=best_cost, trace=trace,
+                        proposals=sum(c.proposals for c in summaries), termination=termination,
+                        chains=list(summaries))
+
+
+def _run_chains(low, params, initial, live, summaries, traces, best, start_err):
+    from .taskgraph import NoRouteError, TaskGraph, _bind, _first_missing_route
+    L = nat.lib()
+    n = len(live)
+    maps = np.zeros((n, low.n_ops), dtype=np.int32)
+    asg = np.zeros((n, low.n_slots), dtype=np.uint8)
+    for i, ci in enumerate(live):
+        low.encode(initial[ci], maps[i], asg[i])
+    seeds = np.array([(params.seed + 1000003 * ci) for ci in live], dtype=object)
+    seeds_u64 = np.array([int(s) % (1 << 64) for s in seeds], dtype=np.uint64)
+    rng_mode = nat.PS_RNG_PHILOX if params.rng == RNG_PHILOX else nat.PS_RNG_MT19937
+    mt = None
+    if rng_mode == nat.PS_RNG_MT19937:
+        mt = np.zeros((n, 625), dtype=np.uint32)
+        for i, s in enumerate(seeds):
+            words, pos = mt_state_words(int(s))
+            mt[i, :624] = words
+            mt[i, 624] = pos
+    deterministic = params.budget_seconds is None
+    cap = int(params.max_proposals) if params.max_proposals is not None else 0
+    record = cap if deterministic else 0
+    mp = nat.PsMcmcParams(rng_mode, params.beta is not None, float(params.beta or 0.0), math.log(10.0),
+                          1 if record else 0, record)
+    h = ctypes.c_void_p()
+    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), n, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds_u64),
+                               nat.ptr(mt) if mt is not None else None, ctypes.byref(h)), "ps_mcmc_create")
+    summ = (nat.PsChainSummary * n)()
+    term = ["budget"] * n
+    try:
+        if deterministic:
+            done = 0
+            while True:
+                step = min(cap - done, max(1, params.segment)) if cap else 0
+                nat.check(L.ps_mcmc_run(h, step, None), "ps_mcmc_run")
+                done += step
+                if done >= cap:
+                    break
+            term = ["proposal-limit"] * n
+        else:
+            t0 = time.monotonic()
+            last_best = np.full(n, np.inf)
+            last_improve = np.full(n, t0)
+            stopped = np.zeros(n, dtype=bool)
+            while True:
+                step = max(1, params.segment)
+                if cap:
+                    step = min(step, cap - int(max((s.proposals for s in summ), default=0)))
+                nat.check(L.ps_mcmc_run(h, max(step, 0), None), "ps_mcmc_run")
+                nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+                now = time.monotonic()
+                halt = np.zeros(n, dtype=np.uint8)
+                for i in range(n):
+                    s = summ[i]
+                    if s.best_cost < last_best[i]:
+                        last_best[i] = s.best_cost
+                        last_improve[i] = now
+                    if stopped[i] or s.status != nat.PS_STATUS_OK:
+                        continue
+                    if cap and s.proposals >= cap:
+                        term[i] = "proposal-limit"
+                    elif now - t0 >= params.budget_seconds:
+                        term[i] = "budget"
+                    elif now - last_improve[i] > max((now - t0) / 2, params.stagnation_floor):
+                        term[i] = "stagnation"
+                    else:
+                        continue
+                    halt[i] = 1
+                    stopped[i] = True
+                if halt.any():
+                    nat.check(L.ps_mcmc_stop(h, nat.ptr(halt)), "ps_mcmc_stop")
+                if stopped.all() or all(summ[i].status not in (nat.PS_STATUS_OK,) or stopped[i] for i in range(n)):
+                    break
+        bmaps = np.zeros((n, low.n_ops), dtype=np.int32)
+        basg = np.zeros((n, low.n_slots), dtype=np.uint8)
+        tc = np.zeros((n, max(record, 1)), dtype=np.float64)
+        tok = np.zeros((n, max(record, 1)), dtype=np.uint8)
+        nat.check(L.ps_mcmc_read(h, summ, nat.ptr(bmaps), nat.ptr(basg), nat.ptr(tc) if record else None,
+                                 nat.ptr(tok) if record else None), "ps_mcmc_read")
+        cur_maps = None
+        for i, ci in enumerate(live):
+            s = summ[i]
+            termination = term[i]
+            if s.status == nat.PS_STATUS_NO_ROUTE:
+                if s.proposals == 0 and not math.isfinite(s.initial_cost):
+                    tg = TaskGraph(low.graph, low.topology, initial[ci].copy(), low.profile, low.mode)
+                    _bind(tg, low)
+                    a, b = _first_missing_route(tg) or ("?", "?")
+                    start_err[ci] = f"error: {NoRouteError(f'no route between device {a} and device {b}')}"
+                    continue
+                # a proposal needed a missing link: the chain's live state holds it
+                a, b = _proposal_route_error(low, h, i, int(s.last_op))
+                termination = f"error: no route between device {a} and device {b}"
+                _logger.warning("chain %d aborted after %d proposals: %s", ci, s.proposals, termination[7:])
+            elif s.status == nat.PS_STATUS_CAPACITY:
+                termination = "error: ready-set capacity exceeded"
+            summaries[ci] = ChainSummary(ci, s.initial_cost, s.best_cost, int(s.proposals), int(s.accepted),
+                                         s.beta, termination)
+            if record:
+                k = min(int(s.proposals), record)
+                traces[ci] = [(float(tc[i, j]), bool(tok[i, j])) for j in range(k)]
+            best[ci] = (s.best_cost, low.decode(bmaps[i], basg[i], template=initial[ci]))
+    finally:
+        L.ps_mcmc_destroy(h)
+
+
+def _proposal_route_error(low, h, i, op_rank):
+    """Device pair the reference's update_task_graph would report for the
+    failing proposal of chain i: predecessor pairs, successor pairs, then the
+    op's rings (taskgraph.py:377-386).  The chain state still holds it."""
+    from .taskgraph import TaskGraph, _bind, _first_missing_route
+    L = nat.lib()
+    n = h_chains = None
+    maps = np.zeros((_mcmc_n(h), low.n_ops), dtype=np.int32)
+    asg = np.zeros((_mcmc_n(h), low.n_slots), dtype=np.uint8)
+    nat.check(L.ps_mcmc_read_state(h, nat.ptr(maps), nat.ptr(asg)), "ps_mcmc_read_state")
+    strat = low.decode(maps[i], asg[i])
+    tg = TaskGraph(low.graph, low.topology, strat, low.profile, low.mode)
+    _bind(tg, low)
+    op_id = low.ops[op_rank]
+    g = low.graph
+    order = [(p, op_id) for p in g.predecessors(op_id)] + [(op_id, s) for s in g.successors(op_id)]
+    return _first_missing_route(tg, pair_order=order, sync_ops=[op_id]) or ("?", "?")
+
+
+def _mcmc_n(h):
+    return int(nat.lib().ps_mcmc_chains(h))
+
+
+def _neighbours(g, topo, maps, devices, op_id, current):
+    for m in maps[op_id]:
+        for assignment in product(devices, repeat=m.size()):
+            if m.degrees == current.degrees and assignment == current.assignment:
+                continue
+            yield ParallelizationConfig(dict(m.degrees), assignment)
+
+
+def _neighbour_batch(low, op_id, base_m, base_a, cfgs):
+    r = low.rank[op_id]
+    off = int(low.slot_off[r])
+    op = low.graph.ops[op_id]
+    mm = np.repeat(base_m[None], len(cfgs), axis=0)
+    aa = np.repeat(base_a[None], len(cfgs), axis=0)
+    for j, (t, assignment) in enumerate(cfgs):
+        mm[j, r] = low.map_index[r][t]
+        for k, dev in enumerate(assignment):
+            aa[j, off + k] = low.dev_index[dev]
+    return _eval_encoded(low, mm, aa)
+
+
+def _greedy_descend(g, topo, profile, strategy, cost, params, batch: int = 4096):
+    """First-improvement hill climb (reference search.py:130-167) with each
+    op's neighbour list evaluated in GPU batches.  A neighbour equal to the
+    op's config at the time it is reached is skipped; after an improvement
+    the scan resumes right after it against the updated strategy -- exactly
+    the reference's sequential semantics."""
+    maps = {oid: enumerate_configs(g.ops[oid], topo, params.max_degree) for oid in sorted(g.ops)}
+    ndev = len(topo.devices)
+    count = sum(ndev ** m.size() for oid in maps for m in maps[oid])
+    if count > params.polish_cap:
+        _logger.info("skipping final descent: %.3g neighbors exceed polish_cap %.3g", count, params.polish_cap)
+        return cost, strategy
+    devices = topo.device_ids()
+    low = lower(g, topo, profile, params.mode, max_degree=params.max_degree, strategies=[strategy],
+                device=params.device)
+    current = strategy.copy()
+    base_m, base_a = low.encode(current)
+    best = float(_eval_encoded(low, base_m[None], base_a[None], [current])[0])
+    improved = True
+    while improved:
+        improved = False
+        for op_id in sorted(g.ops):
+            op = g.ops[op_id]
+            cur = current.configs[op_id]
+            cur_key = (degree_tuple(op, cur.degrees), tuple(cur.assignment))
+            full = [(degree_tuple(op, m.degrees), a, m) for m in maps[op_id]
+                    for a in product(devices, repeat=m.size())]
+            pos = 0
+            while pos < len(full):
+                stop = min(len(full), pos + batch)
+                idx = [i for i in range(pos, stop) if (full[i][0], full[i][1]) != cur_key]
+                if not idx:
+                    pos = stop
+                    continue
+                base_m, base_a = low.encode(current)
+                costs = _neighbour_batch(low, op_id, base_m, base_a, [(full[i][0], full[i][1]) for i in idx])
+                hit = np.nonzero(costs < best)[0]
+                if hit.size == 0:
+                    pos = stop
+                    continue
+                j = int(hit[0])
+                i = idx[j]
+                best = float(costs[j])
+                t, a, m = full[i]
+                current.configs[op_id] = ParallelizationConfig(dict(m.degrees), a)
+                cur_key = (t, a)
+                improved = True
+                pos = i + 1
+    return best, ParallelizationStrategy(dict(current.configs))
+
+
+# -----------------------------------------------------------------------------
+# validation drivers
+
+@dataclass
+class ExhaustiveResult:
+    strategy: ParallelizationStrategy
+    cost: float
+    visited: int
+    space_estimate: float
+
+
+def local_optimality_check(strategy: ParallelizationStrategy, g: OperatorGraph, topo: DeviceTopology,
+                           profile: CostProfile, max_degree: int = 4, cap: float = 5e6, mode: str = MODE_FORWARD,
+                           batch: int = 4096):
+    """First strictly improving single-op neighbour, or None (search.py:408-438);
+    neighbours are scored in GPU batches in the reference's scan order."""
+    devices = topo.device_ids()
+    ndev = len(devices)
+    maps = {oid: enumerate_configs(g.ops[oid], topo, max_degree) for oid in sorted(g.ops)}
+    count = sum(ndev ** m.size() for oid in maps for m in maps[oid])
+    if count > cap:
+        raise SearchSpaceTooLarge(f"{count:.3g} neighbors exceed cap {cap:.3g}")
+    low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=[strategy])
+    base_m, base_a = low.encode(strategy)
+    base = float(_eval_encoded(low, base_m[None], base_a[None], [strategy])[0])
+    for op_id in sorted(g.ops):
+        op = g.ops[op_id]
+        cur = strategy.configs[op_id]
+        gen = ((degree_tuple(op, m.degrees), a, m) for m in maps[op_id] for a in product(devices, repeat=m.size())
+               if not (m.degrees == cur.degrees and a == cur.assignment))
+        while True:
+            chunk = list(islice(gen, batch))
+            if not chunk:
+                break
+            costs = _neighbour_batch(low, op_id, base_m, base_a, [(t, a) for t, a, _ in chunk])
+            hit = np.nonzero(costs < base)[0]
+            if hit.size:
+                j = int(hit[0])
+                t, a, m = chunk[j]
+                return op_id, ParallelizationConfig(dict(m.degrees), a), float(costs[j])
+    return None
+
+
+def exhaustive_optimal(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile, max_degree: int = 4,
+                       cap: float = 1e9, mode: str = MODE_FORWARD) -> ExhaustiveResult:
+    """Not yet on the GPU path."""
+    raise NotImplementedError("exhaustive_optimal is a next-row item on the B200 path (see DESIGN.md)")

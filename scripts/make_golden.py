@@ -1,0 +1,150 @@
+#!/usr/bin/env python3
+"""Generate tests/golden/*.json from the REFERENCE implementation itself.
+
+Run in the build container only (needs the read-only reference checkout):
+
+    PYTHONDONTWRITEBYTECODE=1 python scripts/make_golden.py
+
+Every fixture carries its inputs as the reference's own JSON documents
+(formats.py FORMAT_VERSION 1) so the tests can rebuild identical inputs on a
+machine without the reference, and the outputs the reference produced:
+makespans / counts / timelines as float.hex, MCMC chain summaries and traces
+(unmodified MT19937 and with PhiloxRandom injected as the module's Random).
+"""
+
+import json
+import os
+import random
+import sys
+import types
+
+REF = "/root/reference/pkg"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, os.path.join(REF, "tests"))
+sys.path.insert(0, ROOT)
+
+import parasim as R  # noqa: E402  (the reference)
+import parasim.search as RS  # noqa: E402
+from helpers import random_graph, random_topology  # noqa: E402  (reference test helpers)
+
+from paper_1807_05358_b200.rng import PhiloxRandom  # noqa: E402  (stream under test)
+from paper_1807_05358_b200 import workloads as W  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+H = float.hex
+
+
+def sim_record(g, topo, strategy, mode, with_timeline=True):
+    prof = R.CostProfile()
+    tg = R.build_task_graph(g, topo, strategy, prof, mode)
+    res = R.full_simulate(tg)
+    rec = {"makespan": H(res.makespan), "oracle_makespan": H(R.oracle_simulate(tg)),
+           "tasks": len(tg.tasks), "comm_tasks": sum(1 for t in tg.tasks.values() if t.kind == "comm"),
+           "edges": sum(len(t.outputs) for t in tg.tasks.values()),
+           "comm_bytes": H(float(tg.total_comm_bytes))}
+    if with_timeline:
+        rec["timeline"] = sorted([list(map(str, o)), H(s), H(e), d] for o, (s, e, d) in R.timeline_table(tg).items())
+    return rec
+
+
+def case_doc(g, topo, strategies, mode, md=None):
+    return {"graph": R.graph_to_json(g), "topology": R.topology_to_json(topo), "mode": mode, "max_degree": md,
+            "strategies": [R.strategy_to_json(s) for s in strategies]}
+
+
+def simulate_cases():
+    cases = []
+    for seed in range(40):
+        rng = random.Random(50000 + seed)
+        g = random_graph(rng, 4, 14)
+        topo = random_topology(rng, rng.choice((2, 4, 8, 16)))
+        mode = R.MODE_FULL if seed % 2 else R.MODE_FORWARD
+        md = rng.choice((2, 3, 4))
+        strategies = [R.data_parallel_strategy(g, topo)] + [R.random_strategy(g, topo, md, seed * 10 + i)
+                                                           for i in range(3)]
+        doc = case_doc(g, topo, strategies, mode, md)
+        doc["results"] = [sim_record(g, topo, s, mode) for s in strategies]
+        cases.append(doc)
+    return cases
+
+
+def benchmark_cases():
+    out = []
+    specs = [("alexnet_like", W.alexnet_like(), W.single_node_topology(4), 4),
+             ("inception_v3", W.inception_v3(), W.multi_node_topology(4, 4), 4),
+             ("nmt_like_8", W.nmt_like(steps=8, layers=2, batch=64, hidden=1024, vocab=32768),
+              W.multi_node_topology(4, 4), 8)]
+    for name, g0, t0, md in specs:
+        # round-trip through the reference's own formats so both sides read identical docs
+        g = R.graph_from_json(W_json(g0))
+        topo = R.topology_from_json(W_topo_json(t0))
+        strategies = [R.data_parallel_strategy(g, topo)] + [R.random_strategy(g, topo, md, s) for s in range(2)]
+        for mode in (R.MODE_FORWARD, R.MODE_FULL):
+            doc = case_doc(g, topo, strategies, mode, md)
+            doc["name"] = name
+            doc["results"] = [sim_record(g, topo, s, mode, with_timeline=False) for s in strategies]
+            out.append(doc)
+    return out
+
+
+def W_json(g):
+    from paper_1807_05358_b200.formats import graph_to_json
+    return graph_to_json(g)
+
+
+def W_topo_json(t):
+    from paper_1807_05358_b200.formats import topology_to_json
+    return topology_to_json(t)
+
+
+def mcmc_cases():
+    out = []
+    for seed in range(6):
+        rng = random.Random(70000 + seed)
+        g = random_graph(rng, 4, 10)
+        topo = random_topology(rng, rng.choice((2, 4, 8)))
+        mode = R.MODE_FULL if seed % 2 else R.MODE_FORWARD
+        md = rng.choice((2, 4))
+        init = [R.data_parallel_strategy(g, topo), R.random_strategy(g, topo, md, seed)]
+        for rng_name in ("mt19937", "philox"):
+            RS.random = types.SimpleNamespace(Random=PhiloxRandom) if rng_name == "philox" else random
+            try:
+                rep = R.mcmc_search(g, topo, R.CostProfile(), R.SearchParams(
+                    max_proposals=100, seed=seed, max_degree=md, mode=mode, initial=init, polish=False))
+            finally:
+                RS.random = random
+            doc = case_doc(g, topo, init, mode, md)
+            doc.update({"rng": rng_name, "seed": seed, "max_proposals": 100,
+                        "chains": [[H(c.initial_cost), H(c.best_cost), c.proposals, c.accepted, H(c.beta),
+                                    c.termination] for c in rep.chains],
+                        "trace": [[i, H(c), bool(a)] for i, c, a in rep.trace],
+                        "best_cost": H(rep.best_cost),
+                        "best_strategy": R.strategy_to_json(rep.best_strategy)})
+            out.append(doc)
+    return out
+
+
+def rnn3_case():
+    g = R.rnn3()
+    topo = R.single_node_topology(gpus=3)
+    s = R.rnn3_model_parallel_strategy(g, topo)
+    doc = case_doc(g, topo, [s], R.MODE_FORWARD)
+    doc["results"] = [sim_record(g, topo, s, R.MODE_FORWARD)]
+    with open(os.path.join(REF, "tests", "data", "rnn3_model_parallel.json")) as fh:
+        doc["reference_fixture"] = json.load(fh)
+    return doc
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    docs = {"rnn3_model_parallel.json": rnn3_case(), "simulate_random.json": simulate_cases(),
+            "simulate_benchmarks.json": benchmark_cases(), "mcmc.json": mcmc_cases()}
+    for name, doc in docs.items():
+        with open(os.path.join(OUT, name), "w") as fh:
+            json.dump(doc, fh, separators=(",", ":"))
+        print("wrote", name, os.path.getsize(os.path.join(OUT, name)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,153 @@
+"""GPU parity: every makespan / timeline / trajectory bit-identical to the C
+oracle (itself pinned to the reference by tests/golden)."""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+import paper_1807_05358_b200 as ps
+from helpers import manual_task_graph, random_graph, random_topology
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_case(seed):
+    rng = random.Random(seed)
+    g = random_graph(rng, 4, 14)
+    topo = random_topology(rng, rng.choice((2, 4, 8, 16)))
+    mode = ps.MODE_FULL if seed % 2 else ps.MODE_FORWARD
+    md = rng.choice((2, 3, 4))
+    return g, topo, mode, md
+
+
+def test_batch_makespans_match_oracle_on_random_graphs(oracle):
+    for seed in range(60):
+        g, topo, mode, md = _random_case(seed)
+        prof = ps.CostProfile()
+        strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, seed * 100 + i)
+                                                            for i in range(8)]
+        got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=md)
+        want = oracle.makespans(g, topo, prof, mode, strategies)
+        assert list(got) == list(want), seed
+
+
+def test_timelines_match_oracle(oracle):
+    for seed in range(25):
+        g, topo, mode, md = _random_case(1000 + seed)
+        prof = ps.CostProfile()
+        s = ps.random_strategy(g, topo, md, seed)
+        tg = ps.build_task_graph(g, topo, s, prof, mode)
+        res = ps.full_simulate(tg)
+        ref = oracle.simulate(g, topo, prof, mode, s)
+        assert res.makespan == ref["makespan"]
+        assert len(tg.tasks) == ref["tasks"]
+        assert tg.total_comm_bytes == ref["comm_bytes"]
+        assert sum(len(t.outputs) for t in tg.tasks.values()) == ref["edges"]
+        tt = ps.timeline_table(tg)
+        for origin, (start, end, dev) in tt.items():
+            r = ref["timeline"][origin]
+            assert (start, end) == (r[1], r[2]), origin
+
+
+def test_rnn3_golden_fixture():
+    g = ps.rnn3()
+    topo = ps.single_node_topology(gpus=3)
+    tg = ps.build_task_graph(g, topo, ps.rnn3_model_parallel_strategy(g, topo), ps.CostProfile(),
+                             ps.MODE_FORWARD)
+    comm = sum(1 for t in tg.tasks.values() if t.kind == "comm")
+    assert (len(tg.tasks), len(tg.tasks) - comm, comm) == (12, 8, 4)
+    assert sum(len(t.outputs) for t in tg.tasks.values()) == 11
+    assert tg.total_comm_bytes == 16384.0
+    assert ps.full_simulate(tg).makespan == 3.5826560000000005e-06
+    assert ps.oracle_simulate(tg) == 3.5826560000000005e-06
+
+
+def test_scheduler_known_answers():
+    tg, ids = manual_task_graph([("a", "d0", 1.0), ("b", "d0", 2.0), ("c", "d0", 3.0)], [("a", "b"), ("b", "c")])
+    res = ps.full_simulate(tg)
+    assert res.makespan == 6.0
+    assert [tg.timeline[ids[n]].start for n in "abc"] == [0.0, 1.0, 3.0]
+    tg, _ = manual_task_graph([("a", "d0", 5.0), ("b", "d1", 5.0)], [])
+    assert ps.full_simulate(tg).makespan == 5.0
+    tg, ids = manual_task_graph([("src", "d0", 1.0), ("fast", "d0", 1.0), ("slow", "d1", 3.0), ("join", "d0", 1.0)],
+                                [("src", "fast"), ("src", "slow"), ("fast", "join"), ("slow", "join")])
+    res = ps.full_simulate(tg)
+    assert tg.timeline[ids["join"]].ready == 4.0 and res.makespan == 5.0
+    tg, ids = manual_task_graph([("z", "d0", 1.0), ("m", "d0", 1.0), ("a", "d0", 1.0)], [])
+    ps.full_simulate(tg)
+    assert sorted("zma", key=lambda n: tg.timeline[ids[n]].start) == sorted("zma")
+    tg, ids = manual_task_graph([("a", "d0", 3.0), ("hog", "d1", 4.0), ("b", "d1", 1.0)], [("a", "b")])
+    ps.full_simulate(tg)
+    e = tg.timeline[ids["b"]]
+    assert (e.ready, e.start, e.end) == (3.0, 4.0, 5.0)
+
+
+def test_delta_tracks_chained_changes_exactly(oracle):
+    for seed in range(8):
+        g, topo, mode, md = _random_case(2000 + seed)
+        prof = ps.CostProfile()
+        rng = random.Random(seed)
+        tg = ps.build_task_graph(g, topo, ps.random_strategy(g, topo, md, seed), prof, mode)
+        ps.full_simulate(tg)
+        for step in range(12):
+            op_id = rng.choice(sorted(g.ops))
+            cfg = rng.choice(ps.enumerate_configs(g.ops[op_id], topo, md))
+            asg = tuple(rng.choice(topo.device_ids()) for _ in range(cfg.size()))
+            _, changed = ps.update_task_graph(tg, g, topo, op_id, ps.ParallelizationConfig(dict(cfg.degrees), asg))
+            res = ps.delta_simulate(tg, changed)
+            fresh = ps.build_task_graph(g, topo, tg.strategy, prof, mode)
+            assert res.makespan == ps.full_simulate(fresh).makespan
+            assert ps.timeline_table(tg) == ps.timeline_table(fresh)
+            assert res.makespan == oracle.simulate(g, topo, prof, mode, tg.strategy)["makespan"]
+
+
+@pytest.mark.parametrize("rng_mode", ["mt19937", "philox"])
+def test_mcmc_trajectories_match_oracle(oracle, rng_mode):
+    for seed in range(10):
+        g, topo, mode, md = _random_case(3000 + seed)
+        prof = ps.CostProfile()
+        init = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, seed + i) for i in range(3)]
+        params = ps.SearchParams(max_proposals=120, seed=seed, max_degree=md, mode=mode, initial=init,
+                                 polish=False, rng=rng_mode)
+        rep = ps.mcmc_search(g, topo, prof, params)
+        ref = oracle.mcmc(g, topo, prof, mode, init, [seed + 1000003 * c for c in range(4)], 120, md,
+                          rng_mode="mt" if rng_mode == "mt19937" else "philox")
+        for ci, ch in enumerate(rep.chains):
+            s = ref["summary"][ci]
+            assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted, ch.beta) == tuple(s[:5]), (seed, ci)
+            tr = [c for _, c, _ in rep.trace[ci * 120:(ci + 1) * 120]]
+            ok = [a for _, _, a in rep.trace[ci * 120:(ci + 1) * 120]]
+            assert tr == list(ref["cand"][ci]) and ok == [bool(x) for x in ref["ok"][ci]], (seed, ci)
+
+
+def test_benchmark_shapes_match_oracle(oracle):
+    cases = [(ps.alexnet_like(), ps.single_node_topology(4), 4),
+             (ps.inception_v3(), ps.multi_node_topology(4, 4), 4),
+             (ps.nmt_like(steps=4, layers=2, batch=64, hidden=64, vocab=64), ps.multi_node_topology(4, 4), 4)]
+    for g, topo, md in cases:
+        prof = ps.CostProfile()
+        strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, s) for s in range(4)]
+        for mode in (ps.MODE_FORWARD, ps.MODE_FULL):
+            got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=md)
+            want = oracle.makespans(g, topo, prof, mode, strategies)
+            assert list(got) == list(want)
+
+
+def test_missing_link_is_reported_like_the_reference():
+    g = ps.OperatorGraph()
+    g.add_op(ps.Operation("a", ps.OperatorKind("MatMul"), (ps.shape(("sample", 4), ("channel", 8)),),
+                          ps.shape(("sample", 4), ("channel", 8)), param_bytes=256))
+    g.add_op(ps.Operation("b", ps.OperatorKind("MatMul"), (ps.shape(("sample", 4), ("channel", 8)),),
+                          ps.shape(("sample", 4), ("channel", 4)), param_bytes=128))
+    g.add_tensor("a", "b")
+    topo = ps.DeviceTopology()
+    for d in ("d0", "d1", "d2"):
+        topo.add_device(d)
+    topo.add_connection("d0", "d1", 1e9, 0.0)
+    strat = ps.ParallelizationStrategy({
+        "a": ps.ParallelizationConfig({"sample": 1, "channel": 1}, ("d0",)),
+        "b": ps.ParallelizationConfig({"sample": 1, "channel": 1}, ("d2",))})
+    with pytest.raises(ps.NoRouteError, match="no route between device d0 and device d2"):
+        ps.build_task_graph(g, topo, strat, ps.CostProfile(), ps.MODE_FORWARD)
