@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--chains", type=int, default=1024, help="chains per GPU")
-    ap.add_argument("--proposals", type=int, default=16, help="proposals per chain per step")
+    ap.add_argument("--proposals", type=int, default=16, help="proposals per chain per step (--budget-ms 0)")
+    ap.add_argument("--budget-ms", type=float, default=100.0,
+                    help="time-boxed steps: each chain proposes until this much device time has passed")
     ap.add_argument("--mode", default="full-iteration", choices=("forward", "full-iteration"))
     ap.add_argument("--config", default="inception", choices=("inception", "alexnet", "resnet", "nmt", "random"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -138,10 +140,13 @@ def cpu_baseline(g, topo, prof, mode, md, init, seeds, seconds, threads):
     from oracle.oracle_io import Oracle
     orc = Oracle()
     n = min(len(init), threads)
-    t0 = time.perf_counter()
-    orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], 1, md, rng_mode="philox", threads=threads)
-    per_prop = max(1e-6, (time.perf_counter() - t0))  # one full eval + one proposal per chain, in parallel
-    props = max(1, int(seconds / (2 * per_prop)))
+    times = []
+    for p in (1, 3):  # two calibration points: the slope is the per-proposal cost
+        t0 = time.perf_counter()
+        orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], p, md, rng_mode="philox", threads=threads)
+        times.append(time.perf_counter() - t0)
+    per_prop = max(1e-6, (times[1] - times[0]) / 2)
+    props = max(2, int(seconds / per_prop))
     t0 = time.perf_counter()
     out = orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], props, md, rng_mode="philox", threads=threads)
     dt = time.perf_counter() - t0
@@ -212,10 +217,18 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     sh = ctypes.c_void_p(stream.cuda_stream)
     P = args.proposals
+    budget_ns = int(args.budget_ms * 1e6)
+
+    def run_step(handle):
+        if budget_ns:
+            nat.check(L.ps_mcmc_run_budget(handle, 1 << 30, budget_ns, sh), "ps_mcmc_run_budget")
+        else:
+            nat.check(L.ps_mcmc_run(handle, P, sh), "ps_mcmc_run")
+
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     # first launch also scores the initial strategies (warm-up)
     for _ in range(args.warmup):
-        nat.check(L.ps_mcmc_run(h, P, sh), "ps_mcmc_run")
+        run_step(h)
         flush.zero_()
     torch.cuda.synchronize(dev)
     # algorithmic bytes per evaluation: 32 B per task + 4 B per dependency, averaged
@@ -245,7 +258,7 @@ def run_ours(args):
     with ClockSampler(local) as clocks:
         for i in range(args.steps):
             starts[i].record(stream)
-            nat.check(L.ps_mcmc_run(h, P, sh), "ps_mcmc_run")
+            run_step(h)
             ends[i].record(stream)
             flush.zero_()  # L2 flush between timed steps (outside the events)
         torch.cuda.synchronize(dev)
@@ -287,7 +300,7 @@ def run_ours(args):
         h2 = ctypes.c_void_p()
         nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
                                    ctypes.byref(h2)), "ps_mcmc_create")
-        nat.check(L.ps_mcmc_run(h2, P, sh), "ps_mcmc_run")
+        run_step(h2)
         s2 = (nat.PsChainSummary * C)()
         nat.check(L.ps_mcmc_read(h2, s2, nat.ptr(best_maps), nat.ptr(best_asg), None, None), "ps_mcmc_read")
         dt = time.perf_counter() - t0
@@ -310,7 +323,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "mode": args.mode, "max_degree": md, "chains_per_gpu": C,
-                   "proposals_per_chain_per_step": P, "rng": "philox", "l2": "flushed between steps (256 MB write)",
+                   "step": (f"time-boxed: every chain proposes for {args.budget_ms:g} ms of device time"
+                            if budget_ns else f"{P} proposals per chain"),
+                   "proposals_per_step": round(evals / args.steps, 1),
+                   "rng": "philox", "l2": "flushed between steps (256 MB write)",
                    "tasks_per_eval": round(T_avg, 1), "deps_per_eval": round(E_avg, 1),
                    "ready_capacity": info.ready_capacity, "overlap_entries": info.n_entries},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

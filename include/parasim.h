@@ -175,6 +175,10 @@ int ps_mcmc_create(ps_problem *prob, const ps_mcmc_params *params, int n_chains,
 /* Advance every live chain by `proposals` proposals (first call also scores
  * the initial strategies).  Device-resident; asynchronous on `stream`. */
 int ps_mcmc_run(ps_mcmc *m, int proposals, void *stream);
+/* Time-boxed segment: every chain proposes until `max_proposals` or until
+ * budget_ns of device time (%globaltimer) has passed since the launch began,
+ * checked between proposals -- no warp idles behind a slow chain. */
+int ps_mcmc_run_budget(ps_mcmc *m, int max_proposals, uint64_t budget_ns, void *stream);
 int ps_mcmc_read(ps_mcmc *m, ps_chain_summary *summary, int32_t *best_map, uint8_t *best_assign,
                  double *trace_cand, uint8_t *trace_ok);
 /* Number of chains, and their live (current) strategies. */

@@ -114,6 +114,7 @@ def lib():
     L.ps_mcmc_create.argtypes = [vp, ctypes.POINTER(PsMcmcParams), ctypes.c_int, vp, vp, vp, vp,
                                  ctypes.POINTER(vp)]
     L.ps_mcmc_run.argtypes = [vp, ctypes.c_int, vp]
+    L.ps_mcmc_run_budget.argtypes = [vp, ctypes.c_int, ctypes.c_uint64, vp]
     L.ps_mcmc_read.argtypes = [vp, vp, vp, vp, vp, vp]
     L.ps_mcmc_stop.argtypes = [vp, vp]
     L.ps_mcmc_chains.argtypes = [vp]

@@ -588,21 +588,567 @@ overflow:
   return out;
 }
 
-constexpr int WARPS_PER_BLOCK = 4;
+// ================================================================ v2 simulator
+// Latency-optimised replay used by k_simulate_batch and k_mcmc.
+//
+//  * Static per-op / per-pair / per-link tables are staged once per block in
+//    shared memory; the candidate's degree maps, devices, per-pair combo bases,
+//    queue clocks and ready set live in the warp's shared-memory slice, so the
+//    only global reads on the critical path are the overlap rows/columns.
+//  * Tasks get dense slots per candidate (fbase[o] + k), so the per-task
+//    ready/remaining state of typical strategies also fits in shared memory
+//    (larger candidates fall back to a global scratch slice).
+//  * Conservative lookahead: with LB = min over the ready set of ready+exe,
+//    no task that is not yet ready can become ready before LB (end >= ready +
+//    exe).  Every ready task u with ready_u < LB therefore pops before any
+//    future task, and the heap pops them in (ready, origin) order.  A round
+//    takes, per queue, the minimum-key such task (plus the global minimum),
+//    up to 32 of them on distinct queues, and runs them in parallel: each is
+//    the next task of its queue in the reference's pop order, so start =
+//    max(ready, clock[q]) is exactly the reference's value.
+//    (simulate.py:88-107; proof sketch in DESIGN.md "Lookahead rounds".)
 
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
-k_simulate_batch(DevProb P, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
-                 double *makespan, int *status, char *scratch) {
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct Tab {  // block-shared copies of small static tables
+  int *op_slot_off, *op_map_off, *op_in_off, *op_in_pairs, *op_out_off, *op_out_pairs, *op_param_mask;
+  int *pair_src, *pair_dst, *combo_off, *dev_kind, *link_of;
+  double *link_lat, *link_bw;
+};
+
+struct Lay {  // byte offsets / sizes shared by host and device
+  size_t tab_bytes, warp_bytes;
+  int S;  // dense-slot capacity of the shared-memory state
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline size_t tab_bytes_of(const DevProb &P) {
+  size_t b = 0;
+  b += al16(4 * (size_t)(P.n_ops + 1)) * 4;          // slot_off, map_off, in_off, out_off
+  b += al16(4 * (size_t)(P.n_pairs + 1)) * 5;        // in_pairs, out_pairs, src, dst, combo_off
+  b += al16(4 * (size_t)P.n_ops);                    // param mask
+  b += al16(4 * (size_t)P.n_dev) + al16(4 * (size_t)P.n_dev * P.n_dev);
+  b += al16(8 * (size_t)(P.n_links + 1)) * 2;
+  return b;
+}
+
+__host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int S) {
+  size_t b = 0;
+  b += al16(4 * (size_t)P.n_ops) * 2;                // mapl, gmap
+  b += al16(4 * (size_t)(P.n_ops + 1));              // fbase
+  b += al16(4 * (size_t)P.n_pairs) * 2;              // prow, pcol
+  b += al16((size_t)P.n_slots);                      // asg
+  b += al16(8 * (size_t)P.n_queues) * 3;             // qclock, qready, qbest
+  b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap);  // ready set: hi, lo, exe, q
+  b += al16(8 * (size_t)3 * S) + al16(4 * (size_t)3 * S) + al16(8 * (size_t)S);  // state + masks
+  b += 256 + 16;  // proposal staging (old assignment of the changed op)
+  return b;
+}
+
+struct W2 {
+  int *mapl, *gmap, *fbase, *prow, *pcol;
+  unsigned char *asg;
+  double *qclock;
+  unsigned long long *qready, *qbest, *rhi, *rlo;
+  double *rexe;
+  int *rq;
+  double *sready;
+  int *srem;
+  unsigned long long *gmask;
+  unsigned char *oldasg;
+};
+
+__device__ inline void carve_tab(char *base, const DevProb &P, Tab &t) {
+  char *p = base;
+  auto take = [&](size_t bytes) { char *r = p; p += al16(bytes); return r; };
+  t.op_slot_off = (int *)take(4 * (P.n_ops + 1));
+  t.op_map_off = (int *)take(4 * (P.n_ops + 1));
+  t.op_in_off = (int *)take(4 * (P.n_ops + 1));
+  t.op_out_off = (int *)take(4 * (P.n_ops + 1));
+  t.op_in_pairs = (int *)take(4 * (P.n_pairs + 1));
+  t.op_out_pairs = (int *)take(4 * (P.n_pairs + 1));
+  t.pair_src = (int *)take(4 * (P.n_pairs + 1));
+  t.pair_dst = (int *)take(4 * (P.n_pairs + 1));
+  t.combo_off = (int *)take(4 * (P.n_pairs + 1));
+  t.op_param_mask = (int *)take(4 * P.n_ops);
+  t.dev_kind = (int *)take(4 * P.n_dev);
+  t.link_of = (int *)take(4 * P.n_dev * P.n_dev);
+  t.link_lat = (double *)take(8 * (P.n_links + 1));
+  t.link_bw = (double *)take(8 * (P.n_links + 1));
+}
+
+__device__ inline void load_tab(const DevProb &P, const Tab &t) {
+  int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i <= P.n_ops; i += nt) {
+    t.op_slot_off[i] = P.op_slot_off[i];
+    t.op_map_off[i] = P.op_map_off[i];
+    t.op_in_off[i] = P.op_in_off[i];
+    t.op_out_off[i] = P.op_out_off[i];
+  }
+  int nin = P.op_in_off[P.n_ops], nout = P.op_out_off[P.n_ops];
+  for (int i = tid; i < nin; i += nt) t.op_in_pairs[i] = P.op_in_pairs[i];
+  for (int i = tid; i < nout; i += nt) t.op_out_pairs[i] = P.op_out_pairs[i];
+  for (int i = tid; i < P.n_pairs; i += nt) { t.pair_src[i] = P.pair_src[i]; t.pair_dst[i] = P.pair_dst[i]; }
+  for (int i = tid; i <= P.n_pairs; i += nt) t.combo_off[i] = P.combo_off[i];
+  for (int i = tid; i < P.n_ops; i += nt) t.op_param_mask[i] = P.op_param_mask[i];
+  for (int i = tid; i < P.n_dev; i += nt) t.dev_kind[i] = P.dev_kind[i];
+  for (int i = tid; i < P.n_dev * P.n_dev; i += nt) t.link_of[i] = P.link_of[i];
+  for (int i = tid; i < P.n_links; i += nt) { t.link_lat[i] = P.link_lat[i]; t.link_bw[i] = P.link_bw[i]; }
+}
+
+__device__ inline void carve_warp(char *base, const DevProb &P, int S, W2 &w) {
+  char *p = base;
+  auto take = [&](size_t bytes) { char *r = p; p += al16(bytes); return r; };
+  w.mapl = (int *)take(4 * P.n_ops);
+  w.gmap = (int *)take(4 * P.n_ops);
+  w.fbase = (int *)take(4 * (P.n_ops + 1));
+  w.prow = (int *)take(4 * P.n_pairs);
+  w.pcol = (int *)take(4 * P.n_pairs);
+  w.asg = (unsigned char *)take(P.n_slots);
+  w.qclock = (double *)take(8 * P.n_queues);
+  w.qready = (unsigned long long *)take(8 * P.n_queues);
+  w.qbest = (unsigned long long *)take(8 * P.n_queues);
+  w.rhi = (unsigned long long *)take(8 * P.cap);
+  w.rlo = (unsigned long long *)take(8 * P.cap);
+  w.rexe = (double *)take(8 * P.cap);
+  w.rq = (int *)take(4 * P.cap);
+  w.sready = (double *)take(8 * 3 * S);
+  w.srem = (int *)take(4 * 3 * S);
+  w.gmask = (unsigned long long *)take(8 * S);
+  w.oldasg = (unsigned char *)take(256);
+}
+
+struct State {  // per-candidate dense task state (shared or global)
+  double *ready;
+  int *rem;
+  unsigned long long *gmask;
+  int Tf;
+};
+
+// exe time and queue of a task about to enter the ready set; q < 0 = no route
+__device__ __forceinline__ void task_attrs(const DevProb &P, const Tab &T, const W2 &w, const State &st,
+                                           unsigned long long key, int aux, int &q, double &exe, int &ea, int &eb) {
+  unsigned kind = key_kind(key), a = key_a(key), b = key_b(key), c = key_c(key), d = key_d(key);
+  if (kind == KIND_OP || kind == KIND_OP_BWD) {
+    int dev = w.asg[T.op_slot_off[a] + c];
+    q = dev;
+    exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
+    return;
+  }
+  int da, db;
+  double nb;
+  if (kind == KIND_SYNC) {
+    unsigned long long msk = st.gmask[w.fbase[a] + b];
+    int r = __popcll((long long)msk);
+    da = nth_bit(msk, c % r);
+    db = nth_bit(msk, (c + 1) % r);
+    nb = P.map_shard[w.gmap[a]] / (double)r;
+  } else {
+    da = w.asg[T.op_slot_off[a] + c];
+    db = w.asg[T.op_slot_off[b] + d];
+    nb = (double)P.ent_bytes[aux];
+  }
+  int li = T.link_of[da * P.n_dev + db];
+  if (li < 0) { q = -1; ea = da; eb = db; exe = 0.0; return; }
+  q = P.n_dev + li;
+  exe = T.link_lat[li] + nb / T.link_bw[li];
+}
+
+__device__ __forceinline__ bool push2(bool want, double ready, unsigned long long key, double exe, int q, int &n,
+                                      const DevProb &P, const W2 &w, int lane) {
+  unsigned bm = __ballot_sync(FULLMASK, want);
+  if (!bm) return true;
+  int total = __popc(bm);
+  if (n + total > P.cap) return false;
+  if (want) {
+    int pos = n + __popc(bm & ((1u << lane) - 1u));
+    w.rhi[pos] = (unsigned long long)__double_as_longlong(ready);
+    w.rlo[pos] = key;
+    w.rexe[pos] = exe;
+    w.rq[pos] = q;
+  }
+  n += total;
+  return true;
+}
+
+__device__ __forceinline__ int group_of2(const DevProb &P, int op, int g, int k, int pm) {
+  int nd = P.op_ndim[op];
+  int coords[PS_MAXDIM];
+  for (int i = nd - 1; i >= 0; --i) {
+    int dg = P.map_deg[g * PS_MAXDIM + i];
+    coords[i] = k % dg;
+    k /= dg;
+  }
+  int si = 0;
+  for (int i = 0; i < nd; ++i)
+    if (pm >> i & 1) si = si * P.map_deg[g * PS_MAXDIM + i] + coords[i];
+  return si;
+}
+
+// warp-wide lexicographic min of 64-bit (hi, lo) pairs; returns winning lane
+__device__ __forceinline__ int warp_argmin128(unsigned long long hi, unsigned long long lo, int lane) {
+  unsigned cand = FULLMASK, v, mn;
+  v = (unsigned)(hi >> 32); mn = __reduce_min_sync(FULLMASK, v); cand = __ballot_sync(FULLMASK, v == mn);
+  v = (cand >> lane & 1) ? (unsigned)hi : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+  cand &= __ballot_sync(FULLMASK, v == mn);
+  v = (cand >> lane & 1) ? (unsigned)(lo >> 32) : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+  cand &= __ballot_sync(FULLMASK, v == mn);
+  v = (cand >> lane & 1) ? (unsigned)lo : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+  cand &= __ballot_sync(FULLMASK, v == mn);
+  return __ffs(cand) - 1;
+}
+
+__device__ __forceinline__ unsigned long long warp_min64(unsigned long long x, int lane) {
+  unsigned v = (unsigned)(x >> 32), mn = __reduce_min_sync(FULLMASK, v);
+  bool c = v == mn;
+  unsigned lo = c ? (unsigned)x : 0xffffffffu;
+  unsigned mlo = __reduce_min_sync(FULLMASK, lo);
+  return ((unsigned long long)mn << 32) | mlo;
+}
+
+// Candidate setup: gmap, dense bases, per-pair combo bases, state placement.
+__device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2 &w, int S, char *gscratch, int lane) {
+  // gmap + dense prefix of map sizes
+  int carry = 0;
+  for (int base = 0; base < P.n_ops; base += 32) {
+    int o = base + lane;
+    int sz = 0;
+    if (o < P.n_ops) {
+      int g = T.op_map_off[o] + w.mapl[o];
+      w.gmap[o] = g;
+      sz = P.map_size[g];
+    }
+    int incl = sz;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(FULLMASK, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (o < P.n_ops) w.fbase[o] = carry + incl - sz;
+    carry += __shfl_sync(FULLMASK, incl, 31);
+  }
+  if (lane == 0) w.fbase[P.n_ops] = carry;
+  for (int p = lane; p < P.n_pairs; p += 32) {
+    int s = T.pair_src[p], d = T.pair_dst[p];
+    int nmd = T.op_map_off[d + 1] - T.op_map_off[d];
+    int cc = T.combo_off[p] + w.mapl[s] * nmd + w.mapl[d];
+    w.prow[p] = P.combo_row_off[cc];
+    w.pcol[p] = P.combo_col_off[cc];
+  }
+  State st;
+  st.Tf = carry;
+  if (carry <= S) {
+    st.ready = w.sready; st.rem = w.srem; st.gmask = w.gmask;
+  } else {
+    st.ready = (double *)gscratch;
+    st.rem = (int *)(st.ready + 3 * (size_t)P.n_slots);
+    st.gmask = (unsigned long long *)(st.rem + 3 * (size_t)P.n_slots + 2);
+    st.gmask = (unsigned long long *)(((size_t)st.gmask + 15) & ~(size_t)15);
+  }
+  __syncwarp();
+  return st;
+}
+
+__host__ __device__ inline size_t gscratch_bytes(int n_slots) {
+  return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 4 + 16) + al16((size_t)n_slots * 8) + 128;
+}
+
+__device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, int S, char *gscratch, int lane) {
+  SimOut out;
+  out.makespan = 0.0;
+  out.status = PS_STATUS_OK;
+  out.err_a = out.err_b = -1;
+  State st = setup_candidate(P, T, w, S, gscratch, lane);
+  const int Tf = st.Tf;
+  for (int q = lane; q < P.n_queues; q += 32) { w.qclock[q] = 0.0; w.qready[q] = ~0ull; w.qbest[q] = ~0ull; }
+  if (P.full)
+    for (int s = lane; s < Tf; s += 32) st.gmask[s] = 0ull;
+  __syncwarp();
+  // ---- init: in-degrees, ring membership, sources
+  for (int s = lane; s < Tf; s += 32) {
+    int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
+    int k = s - w.fbase[o];
+    int indeg = 0;
+    for (int i = T.op_in_off[o]; i < T.op_in_off[o + 1]; ++i) {
+      int col = w.pcol[T.op_in_pairs[i]] + k;
+      indeg += P.col_ent_off[col + 1] - P.col_ent_off[col];
+    }
+    st.rem[s] = indeg;
+    st.ready[s] = 0.0;
+    if (P.full) {
+      int outd = 1;
+      for (int i = T.op_out_off[o]; i < T.op_out_off[o + 1]; ++i) {
+        int row = w.prow[T.op_out_pairs[i]] + k;
+        outd += P.row_ent_off[row + 1] - P.row_ent_off[row];
+      }
+      st.rem[Tf + s] = outd;
+      st.ready[Tf + s] = 0.0;
+      int pm = T.op_param_mask[o];
+      if (pm >= 0) {
+        int g = w.gmap[o];
+        int si = group_of2(P, o, g, k, pm);
+        atomicOr(&st.gmask[w.fbase[o] + si], 1ull << w.asg[T.op_slot_off[o] + k]);
+        if (k < P.map_ngroups[g]) {
+          st.rem[2 * Tf + s] = P.map_size[g] / P.map_ngroups[g];
+          st.ready[2 * Tf + s] = 0.0;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  int n = 0;
+  bool okc = true;
+  for (int base = 0; base < Tf; base += 32) {
+    int s = base + lane;
+    bool want = false;
+    unsigned long long key = 0;
+    int q = 0;
+    double exe = 0.0;
+    if (s < Tf && st.rem[s] == 0) {
+      int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
+      key = pack_key(KIND_OP, o, 0, s - w.fbase[o], 0);
+      int ea, eb;
+      task_attrs(P, T, w, st, key, 0, q, exe, ea, eb);
+      want = true;
+    }
+    okc &= push2(want, 0.0, key, exe, q, n, P, w, lane);
+  }
+  __syncwarp();
+  if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
+
+  while (n > 0) {
+    // ---- scan 1: minimum key and LB = min(ready + exe)
+    unsigned long long bh = ~0ull, bl = ~0ull, lb = ~0ull;
+    for (int i = lane; i < n; i += 32) {
+      unsigned long long h = w.rhi[i], l = w.rlo[i];
+      if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; }
+      double e = __longlong_as_double((long long)h) + w.rexe[i];
+      unsigned long long eb = (unsigned long long)__double_as_longlong(e);
+      if (eb < lb) lb = eb;
+    }
+    int wl = warp_argmin128(bh, bl, lane);
+    unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
+    double LB = __longlong_as_double((long long)warp_min64(lb, lane));
+    // ---- scan 2: batch members bid for their queue: per-queue minimum
+    // (ready, origin) -- ready first, then origin among equal ready times
+    for (int i = lane; i < n; i += 32) {
+      unsigned long long h2 = w.rhi[i];
+      if (__longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey) atomicMin(&w.qready[w.rq[i]], h2);
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      unsigned long long h2 = w.rhi[i], k2 = w.rlo[i];
+      int q2 = w.rq[i];
+      if ((__longlong_as_double((long long)h2) < LB || k2 == minkey) && w.qready[q2] == h2)
+        atomicMin(&w.qbest[q2], k2);
+    }
+    __syncwarp();
+    // ---- scan 3: winners (<= 32), one per queue; lane j takes winner j
+    int nw = 0;
+    unsigned long long mykey = 0;
+    double myready = 0.0, myexe = 0.0;
+    int myq = -1;
+    for (int base = 0; base < n && nw < 32; base += 32) {
+      int i = base + lane;
+      bool win = false;
+      unsigned long long k2 = 0, h2 = 0;
+      double e2 = 0.0;
+      int q2 = 0;
+      if (i < n) {
+        k2 = w.rlo[i];
+        q2 = w.rq[i];
+        h2 = w.rhi[i];
+        e2 = w.rexe[i];
+        win = w.qbest[q2] == k2 && w.qready[q2] == h2;
+      }
+      unsigned bm = __ballot_sync(FULLMASK, win);
+      while (bm && nw < 32) {
+        int src = __ffs(bm) - 1;
+        bm &= bm - 1;
+        unsigned long long kk = __shfl_sync(FULLMASK, k2, src);
+        unsigned long long hh = __shfl_sync(FULLMASK, h2, src);
+        double ee = __shfl_sync(FULLMASK, e2, src);
+        int qq = __shfl_sync(FULLMASK, q2, src);
+        if (lane == nw) { mykey = kk; myready = __longlong_as_double((long long)hh); myexe = ee; myq = qq; }
+        if (lane == src) w.rhi[i] = ~0ull;  // taken: compacted away below
+        ++nw;
+      }
+    }
+    __syncwarp();
+    bool mine = lane < nw;
+    if (mine) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; }
+    // ---- compaction
+    int m = 0;
+    for (int base = 0; base < n; base += 32) {
+      int i = base + lane;
+      bool keep = false;
+      unsigned long long h2 = 0, k2 = 0;
+      double e2 = 0.0;
+      int q2 = 0;
+      if (i < n) {
+        h2 = w.rhi[i];
+        keep = h2 != ~0ull;
+        k2 = w.rlo[i]; e2 = w.rexe[i]; q2 = w.rq[i];
+      }
+      unsigned bm = __ballot_sync(FULLMASK, keep);
+      __syncwarp();
+      if (keep) {
+        int pos = m + __popc(bm & ((1u << lane) - 1u));
+        w.rhi[pos] = h2; w.rlo[pos] = k2; w.rexe[pos] = e2; w.rq[pos] = q2;
+      }
+      m += __popc(bm);
+      __syncwarp();
+    }
+    n = m;
+    // ---- run the winners: distinct queues, each its queue's next task
+    double end = 0.0;
+    if (mine) {
+      double clk = w.qclock[myq];
+      double start = myready < clk ? clk : myready;
+      end = start + myexe;
+      w.qclock[myq] = end;
+      if (end > out.makespan) out.makespan = end;
+    }
+    // ---- successors: per-lane iterators, stepped in lockstep
+    unsigned kind = key_kind(mykey), a = key_a(mykey), b = key_b(mykey), c = key_c(mykey), d = key_d(mykey);
+    // iterator state
+    int it_stage = mine ? 0 : 9;  // 0 head, 1 pairs, 2 tail, 9 done
+    int pi = 0, pe = 0, ei = 0, ee = 0, cur_p = 0;
+    int mydev = 0;
+    if (mine && (kind == KIND_OP || kind == KIND_OP_BWD)) mydev = w.asg[T.op_slot_off[a] + c];
+    if (mine) {
+      if (kind == KIND_OP) { pi = T.op_out_off[a]; pe = T.op_out_off[a + 1]; }
+      else if (kind == KIND_OP_BWD) { pi = T.op_in_off[a]; pe = T.op_in_off[a + 1]; }
+    }
+    bool err = false;
+    int ea = -1, eb = -1;
+    while (__any_sync(FULLMASK, it_stage != 9)) {
+      // produce one action per lane
+      int act = 0;  // 0 none, 1 arrive, 2 push
+      int slot = 0;
+      unsigned long long skey = 0;
+      int saux = 0;
+      while (it_stage != 9 && act == 0) {
+        if (it_stage == 0) {
+          it_stage = 1;
+          if (kind == KIND_OP && P.full) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
+          else if (kind == KIND_EDGE) { act = 1; slot = w.fbase[b] + d; skey = pack_key(KIND_OP, b, 0, d, 0); it_stage = 9; }
+          else if (kind == KIND_EDGE_BWD) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); it_stage = 9; }
+          else if (kind == KIND_SYNC) {
+            unsigned long long msk = st.gmask[w.fbase[a] + b];
+            int r = __popcll((long long)msk);
+            it_stage = 9;
+            if ((int)c + 1 < 2 * (r - 1)) { act = 2; skey = pack_key(KIND_SYNC, a, b, c + 1, 0); }
+          }
+        } else if (it_stage == 1) {
+          if (ei < ee) {
+            if (kind == KIND_OP) {
+              int e = ei++;
+              int dp = T.pair_dst[cur_p];
+              int l = P.ent_l[e];
+              int ddev = w.asg[T.op_slot_off[dp] + l];
+              if (ddev == mydev) { act = 1; slot = w.fbase[dp] + l; skey = pack_key(KIND_OP, dp, 0, l, 0); }
+              else { act = 2; skey = pack_key(KIND_EDGE, a, dp, c, l); saux = e; }
+            } else {
+              int e = P.col_ent[ei++];
+              int sp = T.pair_src[cur_p];
+              int kk = P.ent_k[e];
+              int sdev = w.asg[T.op_slot_off[sp] + kk];
+              if (sdev == mydev) { act = 1; slot = Tf + w.fbase[sp] + kk; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); }
+              else { act = 2; skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c); saux = e; }
+            }
+          } else if (pi < pe) {
+            if (kind == KIND_OP) {
+              cur_p = T.op_out_pairs[pi++];
+              int row = w.prow[cur_p] + c;
+              ei = P.row_ent_off[row]; ee = P.row_ent_off[row + 1];
+            } else {
+              cur_p = T.op_in_pairs[pi++];
+              int col = w.pcol[cur_p] + c;
+              ei = P.col_ent_off[col]; ee = P.col_ent_off[col + 1];
+            }
+          } else {
+            it_stage = 2;
+          }
+        } else if (it_stage == 2) {
+          it_stage = 9;
+          if (kind == KIND_OP_BWD && T.op_param_mask[a] >= 0) {
+            int si = group_of2(P, a, w.gmap[a], c, T.op_param_mask[a]);
+            unsigned long long msk = st.gmask[w.fbase[a] + si];
+            if (__popcll((long long)msk) >= 2) {
+              act = 1; slot = 2 * Tf + w.fbase[a] + si; skey = pack_key(KIND_SYNC, a, si, 0, 0);
+            }
+          }
+        }
+      }
+      // arrivals: max(ready), then the last arriver pushes (fence pairs order the RMWs)
+      bool want = false;
+      double pready = 0.0;
+      if (act == 1) {
+        atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(end));
+        __threadfence_block();
+        if (atomicSub(&st.rem[slot], 1) == 1) {
+          __threadfence_block();
+          pready = *(volatile double *)&st.ready[slot];
+          want = true;
+        }
+      } else if (act == 2) {
+        want = true;
+        pready = end;
+      }
+      int q = 0;
+      double exe = 0.0;
+      if (want) {
+        task_attrs(P, T, w, st, skey, saux, q, exe, ea, eb);
+        if (q < 0) { err = true; want = false; }
+      }
+      unsigned bad = __ballot_sync(FULLMASK, err);
+      if (bad) {
+        int srcl = __ffs(bad) - 1;
+        out.status = PS_STATUS_NO_ROUTE;
+        out.err_a = __shfl_sync(FULLMASK, ea, srcl);
+        out.err_b = __shfl_sync(FULLMASK, eb, srcl);
+        return out;
+      }
+      if (!push2(want, pready, skey, exe, q, n, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+    }
+    __syncwarp();
+  }
+  // makespan: max over lanes
+  unsigned long long mb = (unsigned long long)__double_as_longlong(out.makespan);
+  unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
+  unsigned lo = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32) == hi ? (unsigned)mb : 0u);
+  out.makespan = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+  return out;
+}
+
+
+
+__global__ void __launch_bounds__(128)
+k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
+                 double *makespan, int *status, char *gscratch) {
   extern __shared__ __align__(16) char smem[];
-  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  int gw = blockIdx.x * WARPS_PER_BLOCK + wib;
-  int nw = gridDim.x * WARPS_PER_BLOCK;
-  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
-  WarpSmem w = warp_smem_at(smem + wib * wsm, P.n_queues, P.cap);
-  Scratch S = scratch_at(scratch + (size_t)gw * scratch_bytes(P.n_slots), P.n_slots);
+  Tab T;
+  carve_tab(smem, P, T);
+  load_tab(P, T);
+  __syncthreads();
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  W2 w;
+  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay.S, w);
+  int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
+  char *gs = gscratch + (size_t)gw * gscratch_bytes(P.n_slots);
   for (int cand = gw; cand < n; cand += nw) {
-    SimOut o = warp_simulate<false>(P, maps + (size_t)cand * P.n_ops, asgs + (size_t)cand * P.n_slots, S, w, lane,
-                                    nullptr);
+    const int *m = maps + (size_t)cand * P.n_ops;
+    const unsigned char *a = asgs + (size_t)cand * P.n_slots;
+    for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = m[i];
+    for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = a[i];
+    __syncwarp();
+    SimOut o = warp_simulate2(P, T, w, lay.S, gs, lane);
     if (lane == 0) {
       makespan[cand] = o.status == PS_STATUS_OK ? o.makespan : -1.0;
       status[cand] = o.status;
@@ -782,22 +1328,28 @@ struct WarpRng {
   }
 };
 
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
-k_mcmc(DevProb P, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
+__global__ void __launch_bounds__(128)
+k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
-       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *scratch) {
+       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns) {
   extern __shared__ __align__(16) char smem[];
-  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  int chain = blockIdx.x * WARPS_PER_BLOCK + wib;
+  Tab T;
+  carve_tab(smem, P, T);
+  load_tab(P, T);
+  __syncthreads();
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  int chain = blockIdx.x * wpb + wib;
   if (chain >= n_chains) return;
-  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
-  char *mysm = smem + wib * (wsm + (size_t)P.n_slots * 0 + 0);
-  WarpSmem w = warp_smem_at(mysm, P.n_queues, P.cap);
-  Scratch S = scratch_at(scratch + (size_t)chain * scratch_bytes(P.n_slots), P.n_slots);
-  int *map = maps + (size_t)chain * P.n_ops;
-  unsigned char *asg = asgs + (size_t)chain * P.n_slots;
+  W2 w;
+  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay.S, w);
+  char *gs = gscratch + (size_t)chain * gscratch_bytes(P.n_slots);
+  int *gmapl = maps + (size_t)chain * P.n_ops;
+  unsigned char *gasg = asgs + (size_t)chain * P.n_slots;
   ChainState cs = st[chain];
   if (cs.status != PS_STATUS_OK) return;
+  for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = gmapl[i];
+  for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = gasg[i];
+  __syncwarp();
   WarpRng rng;
   rng.mode = rng_mode;
   rng.key = cs.key;
@@ -807,8 +1359,10 @@ k_mcmc(DevProb P, int n_chains, int proposals, int rng_mode, int beta_given, dou
   rng.mt = mt_all ? mt_all + (size_t)chain * 624 : nullptr;
   rng.mti = cs.mti;
   if (rng_mode == PS_RNG_PHILOX && rng.bpos < 4) philox_block(rng.ctr - 1, rng.key, rng.buf);
+  int *bmap = best_maps + (size_t)chain * P.n_ops;
+  unsigned char *basg = best_asgs + (size_t)chain * P.n_slots;
   if (!cs.started) {
-    SimOut o = warp_simulate<false>(P, map, asg, S, w, lane, nullptr);
+    SimOut o = warp_simulate2(P, T, w, lay.S, gs, lane);
     cs.started = 1;
     if (o.status != PS_STATUS_OK) {
       cs.status = o.status; cs.err_a = o.err_a; cs.err_b = o.err_b;
@@ -818,37 +1372,40 @@ k_mcmc(DevProb P, int n_chains, int proposals, int rng_mode, int beta_given, dou
     }
     cs.cost = cs.best = cs.initial = o.makespan;
     cs.beta = beta_given ? beta_param : (o.makespan > 0.0 ? __ddiv_rn(ln10, __dmul_rn(0.05, o.makespan)) : 1.0);
-    for (int i = lane; i < P.n_ops; i += 32) best_maps[(size_t)chain * P.n_ops + i] = map[i];
-    for (int i = lane; i < P.n_slots; i += 32) best_asgs[(size_t)chain * P.n_slots + i] = asg[i];
+    for (int i = lane; i < P.n_ops; i += 32) bmap[i] = w.mapl[i];
+    for (int i = lane; i < P.n_slots; i += 32) basg[i] = w.asg[i];
   }
-  // per-warp staging for the proposal: old config of the op
-  __shared__ unsigned char old_asg_all[WARPS_PER_BLOCK][256];
-  unsigned char *old_asg = old_asg_all[wib];
+  unsigned long long t0 = globaltimer_ns();
   for (int it = 0; it < proposals; ++it) {
+    if (budget_ns) {  // time-boxed segment: stop between proposals once the budget is spent
+      unsigned long long now = __shfl_sync(FULLMASK, globaltimer_ns(), 0);
+      if (now - t0 >= budget_ns) break;
+    }
     // _propose_change (search.py:101-115): op, degree map, one device per task
     int o = (int)rng.below((unsigned)P.n_ops);
     int m = (int)rng.below((unsigned)P.op_nmaps_enum[o]);
     cs.last_op = o;
-    int g = P.op_map_off[o] + m;
+    int g = T.op_map_off[o] + m;
     int size = P.map_size[g];
-    int base = P.op_slot_off[o];
-    int old_m = map[o];
-    int old_size = P.map_size[P.op_map_off[o] + old_m];
+    int base = T.op_slot_off[o];
+    int old_m = w.mapl[o];
+    int old_size = P.map_size[T.op_map_off[o] + old_m];
     bool same = (m == old_m);
-    for (int i = lane; i < old_size; i += 32) old_asg[i] = asg[base + i];
+    for (int i = lane; i < old_size; i += 32) w.oldasg[i] = w.asg[base + i];
     __syncwarp();
     for (int k = 0; k < size; ++k) {
       unsigned dv = rng.below((unsigned)P.n_dev);
-      if (lane == 0) asg[base + k] = (unsigned char)dv;
-      same = same && (k < old_size && old_asg[k] == (unsigned char)dv);
+      same = same && (k < old_size && w.oldasg[k] == (unsigned char)dv);
+      __syncwarp();
+      if (lane == 0) w.asg[base + k] = (unsigned char)dv;
     }
-    if (lane == 0) map[o] = m;
+    if (lane == 0) w.mapl[o] = m;
     __syncwarp();
     double cand;
     if (same) {
       cand = cs.cost;
     } else {
-      SimOut so = warp_simulate<false>(P, map, asg, S, w, lane, nullptr);
+      SimOut so = warp_simulate2(P, T, w, lay.S, gs, lane);
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
         break;
@@ -859,8 +1416,8 @@ k_mcmc(DevProb P, int n_chains, int proposals, int rng_mode, int beta_given, dou
     bool ok;
     if (cand <= cs.cost) ok = true;
     else {
-      double p = exp(__dmul_rn(cs.beta, __dsub_rn(cs.cost, cand)));
-      ok = p >= 1.0 ? true : rng.random() < p;
+      double pr = exp(__dmul_rn(cs.beta, __dsub_rn(cs.cost, cand)));
+      ok = pr >= 1.0 ? true : rng.random() < pr;
     }
     if (trace_cap > 0 && idx < trace_cap && lane == 0) {
       trace_cand[(size_t)chain * trace_cap + idx] = cand;
@@ -868,18 +1425,20 @@ k_mcmc(DevProb P, int n_chains, int proposals, int rng_mode, int beta_given, dou
     }
     if (cand < cs.best) {
       cs.best = cand;
-      for (int i = lane; i < P.n_ops; i += 32) best_maps[(size_t)chain * P.n_ops + i] = map[i];
-      for (int i = lane; i < P.n_slots; i += 32) best_asgs[(size_t)chain * P.n_slots + i] = asg[i];
+      for (int i = lane; i < P.n_ops; i += 32) bmap[i] = w.mapl[i];
+      for (int i = lane; i < P.n_slots; i += 32) basg[i] = w.asg[i];
     }
     if (ok) {
       cs.cost = cand;
       cs.accepted++;
     } else {
-      for (int i = lane; i < old_size; i += 32) asg[base + i] = old_asg[i];
-      if (lane == 0) map[o] = old_m;
+      for (int i = lane; i < old_size; i += 32) w.asg[base + i] = w.oldasg[i];
+      if (lane == 0) w.mapl[o] = old_m;
     }
     __syncwarp();
   }
+  for (int i = lane; i < P.n_ops; i += 32) gmapl[i] = w.mapl[i];
+  for (int i = lane; i < P.n_slots; i += 32) gasg[i] = w.asg[i];
   cs.key = rng.key;
   cs.ctr = rng.ctr;
   cs.bpos = rng.bpos;
@@ -933,8 +1492,9 @@ struct ps_problem {
   DevProb P;
   std::vector<void *> owned;
   long long n_entries, n_combos, n_rows, n_cols;
-  size_t smem_per_block;
-  int blocks_per_sm, sm_count;
+  size_t smem_per_block;  // v2 kernels: tab + wpb * warp slice
+  int blocks_per_sm, sm_count, wpb;
+  Lay lay;
   char *scratch = nullptr;  // batch scratch (grid-sized)
   size_t scratch_warps = 0;
   int *d_map = nullptr;
@@ -1070,18 +1630,46 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   cudaFree(cnt); cudaFree(ccnt); cudaFree(tmp);
-  // ---- launch geometry for the warp-per-candidate kernels
-  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
-  pr->smem_per_block = wsm * WARPS_PER_BLOCK;
-  if (pr->smem_per_block > 48 * 1024) {
-    CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
-    CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
-  }
-  if (wsm > 48 * 1024) CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+  // ---- launch geometry: largest shared-state capacity S that still keeps
+  // >= 8 resident warps (candidates) per SM; warps per block in {4, 2, 1}
   CK(cudaDeviceGetAttribute(&pr->sm_count, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pr->blocks_per_sm, k_simulate_batch, WARPS_PER_BLOCK * 32,
-                                                   pr->smem_per_block));
-  if (pr->blocks_per_sm < 1) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "per-warp shared memory too large"); }
+  int optin = 0, per_sm = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+  {
+    size_t tb = al16(tab_bytes_of(P));
+    const int caps[] = {1 << 30, 1024, 768, 640, 512, 384, 256, 192, 128, 64, 0};
+    int bestS = -1, bestW = 0, bestWarps = 0;
+    for (int ci = 0; ci < (int)(sizeof caps / sizeof caps[0]); ++ci) {
+      int S = std::min(caps[ci], P.n_slots);
+      size_t wb = al16(warp_bytes_of(P, S));
+      int cw = 0, cwp = 0;
+      for (int wp : {4, 2, 1}) {
+        size_t blk = tb + wp * wb;
+        if (blk > (size_t)optin) continue;
+        int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
+        int warps = std::min(64, blocks * wp);
+        if (warps > cw) { cw = warps; cwp = wp; }
+      }
+      if (cw > bestWarps) { bestWarps = cw; bestS = S; bestW = cwp; }
+      if (cw >= 8) { bestWarps = cw; bestS = S; bestW = cwp; break; }
+    }
+    if (bestS < 0) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "problem too large for shared memory"); }
+    pr->lay.tab_bytes = tb;
+    pr->lay.warp_bytes = al16(warp_bytes_of(P, bestS));
+    pr->lay.S = bestS;
+    pr->wpb = bestW;
+    pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
+    pr->blocks_per_sm = std::max(1, bestWarps / bestW);
+  }
+  CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
+  CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
+  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
+  if (wsm > 48 * 1024) CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch, pr->wpb * 32, pr->smem_per_block));
+  if (occ < 1) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "kernel does not fit on an SM"); }
+  pr->blocks_per_sm = occ;
   pr->device_bytes = 0;
   *out = pr;
   return PS_OK;
@@ -1103,7 +1691,7 @@ int ps_problem_info_get(const ps_problem *pr, ps_problem_info *o) {
   o->n_queues = pr->P.n_queues;
   o->n_slots = pr->P.n_slots;
   o->ready_capacity = pr->P.cap;
-  o->warps_per_block = WARPS_PER_BLOCK;
+  o->warps_per_block = pr->wpb;
   o->device_bytes = pr->device_bytes;
   return PS_OK;
 }
@@ -1154,15 +1742,16 @@ int ps_simulate_batch(ps_problem *pr, const int32_t *map_local, const uint8_t *a
     CK(cudaMemcpyAsync(pr->d_asg, assign, (size_t)n * pr->P.n_slots, cudaMemcpyHostToDevice, s));
     dm = pr->d_map; da = pr->d_asg; dk = pr->d_mk; ds = pr->d_st;
   }
-  int blocks = std::min((n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, pr->sm_count * pr->blocks_per_sm);
-  size_t warps = (size_t)blocks * WARPS_PER_BLOCK;
+  int wpb = pr->wpb;
+  int blocks = std::min((n + wpb - 1) / wpb, pr->sm_count * pr->blocks_per_sm);
+  size_t warps = (size_t)blocks * wpb;
   if (warps > pr->scratch_warps) {
     cudaFree(pr->scratch);
-    size_t want = (size_t)pr->sm_count * pr->blocks_per_sm * WARPS_PER_BLOCK;
-    CK(cudaMalloc(&pr->scratch, want * scratch_bytes(pr->P.n_slots)));
+    size_t want = (size_t)pr->sm_count * pr->blocks_per_sm * wpb;
+    CK(cudaMalloc(&pr->scratch, want * gscratch_bytes(pr->P.n_slots)));
     pr->scratch_warps = want;
   }
-  k_simulate_batch<<<blocks, WARPS_PER_BLOCK * 32, pr->smem_per_block, s>>>(pr->P, dm, da, n, dk, ds, pr->scratch);
+  k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch);
   CK(cudaGetLastError());
   if (flags != PS_DEVICE_PTRS) {
     CK(cudaMemcpyAsync(makespan_out, dk, n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1285,7 +1874,7 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
-  CK(cudaMalloc(&m->scratch, (size_t)n * scratch_bytes(P.n_slots)));
+  CK(cudaMalloc(&m->scratch, (size_t)n * gscratch_bytes(P.n_slots)));
   CK(cudaMalloc(&m->d_best, sizeof(double)));
   CK(cudaMalloc(&m->d_bestc, sizeof(int)));
   CK(cudaMemcpy(m->maps, init_map, (size_t)n * P.n_ops * sizeof(int), cudaMemcpyHostToDevice));
@@ -1315,18 +1904,25 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   return PS_OK;
 }
 
-int ps_mcmc_run(ps_mcmc *m, int proposals, void *stream) {
+static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, void *stream) {
   if (!m || proposals < 0) return fail(PS_ERR_INVALID, "bad arguments");
   ps_problem *pr = m->prob;
   CK(cudaSetDevice(pr->device));
-  int blocks = (m->n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+  int wpb = pr->wpb;
+  int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
-  k_mcmc<<<blocks, WARPS_PER_BLOCK * 32, smem, (cudaStream_t)stream>>>(
-      pr->P, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
+  k_mcmc<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
+      pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
-      m->params.record_trace ? m->params.trace_capacity : 0, m->scratch);
+      m->params.record_trace ? m->params.trace_capacity : 0, m->scratch, budget_ns);
   CK(cudaGetLastError());
   return PS_OK;
+}
+
+int ps_mcmc_run(ps_mcmc *m, int proposals, void *stream) { return mcmc_launch(m, proposals, 0ull, stream); }
+
+int ps_mcmc_run_budget(ps_mcmc *m, int max_proposals, uint64_t budget_ns, void *stream) {
+  return mcmc_launch(m, max_proposals, (unsigned long long)budget_ns, stream);
 }
 
 int ps_mcmc_read(ps_mcmc *m, ps_chain_summary *summary, int32_t *best_map, uint8_t *best_assign, double *trace_cand,
