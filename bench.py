@@ -270,17 +270,22 @@ def run_ours(args):
     nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
     evals = sum(s.proposals for s in summ) - props0
     bad = sum(1 for s in summ if s.status != nat.PS_STATUS_OK)
-    # best strategy across chains: device argmin, then the tiny cross-GPU exchange
+    # best strategy across chains: device argmin, then the one cross-GPU exchange
+    from paper_1807_05358_b200.parallel import global_best
     bc, bi = ctypes.c_double(), ctypes.c_int32()
     nat.check(L.ps_mcmc_best(h, ctypes.byref(bc), ctypes.byref(bi)), "ps_mcmc_best")
-    best_local = float(bc.value)
+    bm_all = np.zeros((C, low.n_ops), dtype=np.int32)
+    ba_all = np.zeros((C, low.n_slots), dtype=np.uint8)
+    nat.check(L.ps_mcmc_read(h, None, nat.ptr(bm_all), nat.ptr(ba_all), None, None), "ps_mcmc_read")
+    li = int(bi.value)
+    win_cost, win_chain, win_map, win_asg = global_best(
+        float(bc.value), first + li if li >= 0 else -1, bm_all[max(li, 0)], ba_all[max(li, 0)], device=dev)
     t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     ev = torch.tensor([float(evals)], dtype=torch.float64, device=dev)
-    best = torch.tensor([best_local], dtype=torch.float64, device=dev)
+    best = torch.tensor([win_cost], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
         dist.all_reduce(ev, op=dist.ReduceOp.SUM)
-        dist.all_reduce(best, op=dist.ReduceOp.MIN)
     total_ms = float(t_max.item())
     all_evals = float(ev.item())
     value = all_evals / (total_ms / 1e3)
@@ -335,7 +340,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
-        "chain_failures": bad, "best_makespan": float(best.item()),
+        "chain_failures": bad, "best_makespan": float(best.item()), "best_chain": win_chain,
     }
     L.ps_mcmc_destroy(h)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
