@@ -645,7 +645,9 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int S) {
   b += al16((size_t)P.n_slots);                      // asg
   b += al16(8 * (size_t)P.n_queues) * 3;             // qclock, qready, qbest
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap);  // ready set: hi, lo, exe, q
-  b += al16(8 * (size_t)3 * S) + al16(4 * (size_t)3 * S) + al16(8 * (size_t)S);  // state + masks
+  b += al16(8 * (size_t)3 * S) + al16(4 * (size_t)3 * S) + al16(8 * (size_t)S) + al16((size_t)S);  // state, masks, groups
+  b += al16(4 * (size_t)P.cap);                      // member list
+  b += al16(8 * (size_t)P.n_ops) * 2;                // per-op exe cache (single device kind)
   b += 256 + 16;  // proposal staging (old assignment of the changed op)
   return b;
 }
@@ -660,6 +662,9 @@ struct W2 {
   double *sready;
   int *srem;
   unsigned long long *gmask;
+  unsigned char *sgrp;
+  int *mem;
+  double *exef, *exeb;
   unsigned char *oldasg;
 };
 
@@ -720,6 +725,10 @@ __device__ inline void carve_warp(char *base, const DevProb &P, int S, W2 &w) {
   w.sready = (double *)take(8 * 3 * S);
   w.srem = (int *)take(4 * 3 * S);
   w.gmask = (unsigned long long *)take(8 * S);
+  w.sgrp = (unsigned char *)take(S);
+  w.mem = (int *)take(4 * P.cap);
+  w.exef = (double *)take(8 * P.n_ops);
+  w.exeb = (double *)take(8 * P.n_ops);
   w.oldasg = (unsigned char *)take(256);
 }
 
@@ -727,6 +736,7 @@ struct State {  // per-candidate dense task state (shared or global)
   double *ready;
   int *rem;
   unsigned long long *gmask;
+  unsigned char *grp;  // parameter shard of each forward slot
   int Tf;
 };
 
@@ -737,7 +747,8 @@ __device__ __forceinline__ void task_attrs(const DevProb &P, const Tab &T, const
   if (kind == KIND_OP || kind == KIND_OP_BWD) {
     int dev = w.asg[T.op_slot_off[a] + c];
     q = dev;
-    exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
+    if (P.n_kinds == 1) exe = (kind == KIND_OP ? w.exef : w.exeb)[a];
+    else exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
     return;
   }
   int da, db;
@@ -822,6 +833,7 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
       int g = T.op_map_off[o] + w.mapl[o];
       w.gmap[o] = g;
       sz = P.map_size[g];
+      if (P.n_kinds == 1) { w.exef[o] = P.exe_fwd[g]; w.exeb[o] = P.exe_bwd[g]; }
     }
     int incl = sz;
 #pragma unroll
@@ -843,19 +855,21 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
   State st;
   st.Tf = carry;
   if (carry <= S) {
-    st.ready = w.sready; st.rem = w.srem; st.gmask = w.gmask;
+    st.ready = w.sready; st.rem = w.srem; st.gmask = w.gmask; st.grp = w.sgrp;
   } else {
     st.ready = (double *)gscratch;
     st.rem = (int *)(st.ready + 3 * (size_t)P.n_slots);
     st.gmask = (unsigned long long *)(st.rem + 3 * (size_t)P.n_slots + 2);
     st.gmask = (unsigned long long *)(((size_t)st.gmask + 15) & ~(size_t)15);
+    st.grp = (unsigned char *)(st.gmask + P.n_slots);
   }
   __syncwarp();
   return st;
 }
 
 __host__ __device__ inline size_t gscratch_bytes(int n_slots) {
-  return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 4 + 16) + al16((size_t)n_slots * 8) + 128;
+  return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 4 + 16) + al16((size_t)n_slots * 8) +
+         al16((size_t)n_slots) + 128;
 }
 
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, int S, char *gscratch, int lane) {
@@ -892,6 +906,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
       if (pm >= 0) {
         int g = w.gmap[o];
         int si = group_of2(P, o, g, k, pm);
+        st.grp[s] = (unsigned char)si;
         atomicOr(&st.gmask[w.fbase[o] + si], 1ull << w.asg[T.op_slot_off[o] + k]);
         if (k < P.map_ngroups[g]) {
           st.rem[2 * Tf + s] = P.map_size[g] / P.map_ngroups[g];
@@ -934,77 +949,88 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
     int wl = warp_argmin128(bh, bl, lane);
     unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
     double LB = __longlong_as_double((long long)warp_min64(lb, lane));
-    // ---- scan 2: batch members bid for their queue: per-queue minimum
-    // (ready, origin) -- ready first, then origin among equal ready times
-    for (int i = lane; i < n; i += 32) {
-      unsigned long long h2 = w.rhi[i];
-      if (__longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey) atomicMin(&w.qready[w.rq[i]], h2);
+    // ---- scan 2: members (ready < LB, or the global minimum) -> member list,
+    // and each bids its ready time for its queue
+    int nm = 0;
+    for (int base = 0; base < n; base += 32) {
+      int i = base + lane;
+      bool mem = false;
+      if (i < n) {
+        unsigned long long h2 = w.rhi[i];
+        mem = __longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey;
+        if (mem) atomicMin(&w.qready[w.rq[i]], h2);
+      }
+      unsigned bm = __ballot_sync(FULLMASK, mem);
+      if (mem) w.mem[nm + __popc(bm & ((1u << lane) - 1u))] = i;
+      nm += __popc(bm);
     }
     __syncwarp();
-    for (int i = lane; i < n; i += 32) {
-      unsigned long long h2 = w.rhi[i], k2 = w.rlo[i];
+    // ---- members tied on their queue's ready time bid their origin key
+    for (int j = lane; j < nm; j += 32) {
+      int i = w.mem[j];
       int q2 = w.rq[i];
-      if ((__longlong_as_double((long long)h2) < LB || k2 == minkey) && w.qready[q2] == h2)
-        atomicMin(&w.qbest[q2], k2);
+      if (w.qready[q2] == w.rhi[i]) atomicMin(&w.qbest[q2], w.rlo[i]);
     }
     __syncwarp();
-    // ---- scan 3: winners (<= 32), one per queue; lane j takes winner j
+    // ---- winners: each queue's minimum (ready, origin); lane k holds winner k
     int nw = 0;
     unsigned long long mykey = 0;
     double myready = 0.0, myexe = 0.0;
-    int myq = -1;
-    for (int base = 0; base < n && nw < 32; base += 32) {
-      int i = base + lane;
+    int myq = -1, mypos = -1;
+    for (int base = 0; base < nm && nw < 32; base += 32) {
+      int j = base + lane;
       bool win = false;
-      unsigned long long k2 = 0, h2 = 0;
-      double e2 = 0.0;
-      int q2 = 0;
-      if (i < n) {
-        k2 = w.rlo[i];
-        q2 = w.rq[i];
-        h2 = w.rhi[i];
-        e2 = w.rexe[i];
-        win = w.qbest[q2] == k2 && w.qready[q2] == h2;
+      int i = 0;
+      if (j < nm) {
+        i = w.mem[j];
+        int q2 = w.rq[i];
+        win = w.qbest[q2] == w.rlo[i] && w.qready[q2] == w.rhi[i];
       }
       unsigned bm = __ballot_sync(FULLMASK, win);
-      while (bm && nw < 32) {
-        int src = __ffs(bm) - 1;
-        bm &= bm - 1;
-        unsigned long long kk = __shfl_sync(FULLMASK, k2, src);
-        unsigned long long hh = __shfl_sync(FULLMASK, h2, src);
-        double ee = __shfl_sync(FULLMASK, e2, src);
-        int qq = __shfl_sync(FULLMASK, q2, src);
-        if (lane == nw) { mykey = kk; myready = __longlong_as_double((long long)hh); myexe = ee; myq = qq; }
-        if (lane == src) w.rhi[i] = ~0ull;  // taken: compacted away below
-        ++nw;
+      int rank = __popc(bm & ((1u << lane) - 1u));
+      int slot = nw + rank;
+      // winner at member position -> lane `slot` (ignored beyond 32)
+      for (int src = 0; src < 32; ++src) {
+        if (!(bm >> src & 1)) continue;
+        int s2 = __shfl_sync(FULLMASK, slot, src);
+        int i2 = __shfl_sync(FULLMASK, i, src);
+        if (lane == s2 && s2 < 32) mypos = i2;
       }
+      nw = min(32, nw + __popc(bm));
+    }
+    bool mine = lane < nw;
+    if (mine) {
+      mykey = w.rlo[mypos];
+      myready = __longlong_as_double((long long)w.rhi[mypos]);
+      myexe = w.rexe[mypos];
+      myq = w.rq[mypos];
     }
     __syncwarp();
-    bool mine = lane < nw;
-    if (mine) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; }
-    // ---- compaction
-    int m = 0;
-    for (int base = 0; base < n; base += 32) {
-      int i = base + lane;
-      bool keep = false;
+    if (mine) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rhi[mypos] = ~0ull; }
+    __syncwarp();
+    // ---- remove the winners: refill holes below n-nw with survivors from the tail
+    {
+      int tailpos = n - nw + lane;
+      bool survivor = lane < nw && w.rhi[tailpos] != ~0ull;
+      unsigned sm = __ballot_sync(FULLMASK, survivor);
+      bool head_hole = mine && mypos < n - nw;
+      unsigned hm = __ballot_sync(FULLMASK, head_hole);
+      int hrank = __popc(hm & ((1u << lane) - 1u));
+      int src = -1;
+      if (head_hole) {
+        unsigned x = sm;
+        for (int r = 0; r < hrank; ++r) x &= x - 1;
+        src = n - nw + __ffs(x) - 1;
+      }
       unsigned long long h2 = 0, k2 = 0;
       double e2 = 0.0;
       int q2 = 0;
-      if (i < n) {
-        h2 = w.rhi[i];
-        keep = h2 != ~0ull;
-        k2 = w.rlo[i]; e2 = w.rexe[i]; q2 = w.rq[i];
-      }
-      unsigned bm = __ballot_sync(FULLMASK, keep);
+      if (head_hole) { h2 = w.rhi[src]; k2 = w.rlo[src]; e2 = w.rexe[src]; q2 = w.rq[src]; }
       __syncwarp();
-      if (keep) {
-        int pos = m + __popc(bm & ((1u << lane) - 1u));
-        w.rhi[pos] = h2; w.rlo[pos] = k2; w.rexe[pos] = e2; w.rq[pos] = q2;
-      }
-      m += __popc(bm);
+      if (head_hole) { w.rhi[mypos] = h2; w.rlo[mypos] = k2; w.rexe[mypos] = e2; w.rq[mypos] = q2; }
+      n -= nw;
       __syncwarp();
     }
-    n = m;
     // ---- run the winners: distinct queues, each its queue's next task
     double end = 0.0;
     if (mine) {
@@ -1014,92 +1040,106 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
       w.qclock[myq] = end;
       if (end > out.makespan) out.makespan = end;
     }
-    // ---- successors: per-lane iterators, stepped in lockstep
-    unsigned kind = key_kind(mykey), a = key_a(mykey), b = key_b(mykey), c = key_c(mykey), d = key_d(mykey);
-    // iterator state
-    int it_stage = mine ? 0 : 9;  // 0 head, 1 pairs, 2 tail, 9 done
-    int pi = 0, pe = 0, ei = 0, ee = 0, cur_p = 0;
-    int mydev = 0;
-    if (mine && (kind == KIND_OP || kind == KIND_OP_BWD)) mydev = w.asg[T.op_slot_off[a] + c];
-    if (mine) {
-      if (kind == KIND_OP) { pi = T.op_out_off[a]; pe = T.op_out_off[a + 1]; }
-      else if (kind == KIND_OP_BWD) { pi = T.op_in_off[a]; pe = T.op_in_off[a + 1]; }
+    // ---- successors: lane groups of G per winner, random access into each list
+    int lg = 31 - __clz(nw);           // floor(log2 nw)
+    if ((1 << lg) < nw) ++lg;          // ceil
+    int G = 32 >> lg;
+    int wi = lane / G, j0 = lane % G;
+    bool act_lane = wi < nw;
+    int srcl = act_lane ? wi : 0;
+    unsigned long long wkey = __shfl_sync(FULLMASK, mykey, srcl);
+    double wend = __shfl_sync(FULLMASK, end, srcl);
+    unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
+    int wdev = 0, head = 0, tail = 0, L = 0, ring = 0;
+    if (act_lane) {
+      if (kind == KIND_OP || kind == KIND_OP_BWD) wdev = w.asg[T.op_slot_off[a] + c];
+      if (kind == KIND_OP) {
+        head = P.full ? 1 : 0;
+        L = head;
+        for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
+          int row = w.prow[T.op_out_pairs[i]] + c;
+          L += P.row_ent_off[row + 1] - P.row_ent_off[row];
+        }
+      } else if (kind == KIND_OP_BWD) {
+        for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
+          int col = w.pcol[T.op_in_pairs[i]] + c;
+          L += P.col_ent_off[col + 1] - P.col_ent_off[col];
+        }
+        if (T.op_param_mask[a] >= 0) {
+          int s0 = w.fbase[a] + c;
+          int si = st.grp[s0];
+          if (__popcll((long long)st.gmask[w.fbase[a] + si]) >= 2) { tail = 1; ring = si; }
+        }
+        L += tail;
+      } else if (kind == KIND_SYNC) {
+        int r = __popcll((long long)st.gmask[w.fbase[a] + b]);
+        L = ((int)c + 1 < 2 * (r - 1)) ? 1 : 0;
+      } else {
+        L = 1;
+      }
     }
+    int iters = (L + G - 1) / G;
+    iters = (int)__reduce_max_sync(FULLMASK, (unsigned)(act_lane ? iters : 0));
     bool err = false;
     int ea = -1, eb = -1;
-    while (__any_sync(FULLMASK, it_stage != 9)) {
-      // produce one action per lane
-      int act = 0;  // 0 none, 1 arrive, 2 push
-      int slot = 0;
+    for (int t = 0; t < iters; ++t) {
+      int idx = j0 + t * G;
+      int act = 0;  // 1 arrive, 2 push
+      int slot = 0, saux = 0;
       unsigned long long skey = 0;
-      int saux = 0;
-      while (it_stage != 9 && act == 0) {
-        if (it_stage == 0) {
-          it_stage = 1;
-          if (kind == KIND_OP && P.full) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
-          else if (kind == KIND_EDGE) { act = 1; slot = w.fbase[b] + d; skey = pack_key(KIND_OP, b, 0, d, 0); it_stage = 9; }
-          else if (kind == KIND_EDGE_BWD) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); it_stage = 9; }
-          else if (kind == KIND_SYNC) {
-            unsigned long long msk = st.gmask[w.fbase[a] + b];
-            int r = __popcll((long long)msk);
-            it_stage = 9;
-            if ((int)c + 1 < 2 * (r - 1)) { act = 2; skey = pack_key(KIND_SYNC, a, b, c + 1, 0); }
-          }
-        } else if (it_stage == 1) {
-          if (ei < ee) {
-            if (kind == KIND_OP) {
-              int e = ei++;
-              int dp = T.pair_dst[cur_p];
-              int l = P.ent_l[e];
-              int ddev = w.asg[T.op_slot_off[dp] + l];
-              if (ddev == mydev) { act = 1; slot = w.fbase[dp] + l; skey = pack_key(KIND_OP, dp, 0, l, 0); }
-              else { act = 2; skey = pack_key(KIND_EDGE, a, dp, c, l); saux = e; }
-            } else {
-              int e = P.col_ent[ei++];
-              int sp = T.pair_src[cur_p];
-              int kk = P.ent_k[e];
-              int sdev = w.asg[T.op_slot_off[sp] + kk];
-              if (sdev == mydev) { act = 1; slot = Tf + w.fbase[sp] + kk; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); }
-              else { act = 2; skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c); saux = e; }
-            }
-          } else if (pi < pe) {
-            if (kind == KIND_OP) {
-              cur_p = T.op_out_pairs[pi++];
-              int row = w.prow[cur_p] + c;
-              ei = P.row_ent_off[row]; ee = P.row_ent_off[row + 1];
-            } else {
-              cur_p = T.op_in_pairs[pi++];
-              int col = w.pcol[cur_p] + c;
-              ei = P.col_ent_off[col]; ee = P.col_ent_off[col + 1];
-            }
-          } else {
-            it_stage = 2;
-          }
-        } else if (it_stage == 2) {
-          it_stage = 9;
-          if (kind == KIND_OP_BWD && T.op_param_mask[a] >= 0) {
-            int si = group_of2(P, a, w.gmap[a], c, T.op_param_mask[a]);
-            unsigned long long msk = st.gmask[w.fbase[a] + si];
-            if (__popcll((long long)msk) >= 2) {
-              act = 1; slot = 2 * Tf + w.fbase[a] + si; skey = pack_key(KIND_SYNC, a, si, 0, 0);
+      if (act_lane && idx < L) {
+        if (kind == KIND_OP) {
+          if (idx < head) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
+          else {
+            int r = idx - head;
+            for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
+              int p = T.op_out_pairs[i];
+              int row = w.prow[p] + c;
+              int e0 = P.row_ent_off[row], len = P.row_ent_off[row + 1] - e0;
+              if (r < len) {
+                int e = e0 + r;
+                int dp = T.pair_dst[p];
+                int l = P.ent_l[e];
+                if (w.asg[T.op_slot_off[dp] + l] == wdev) { act = 1; slot = w.fbase[dp] + l; skey = pack_key(KIND_OP, dp, 0, l, 0); }
+                else { act = 2; skey = pack_key(KIND_EDGE, a, dp, c, l); saux = e; }
+                break;
+              }
+              r -= len;
             }
           }
-        }
+        } else if (kind == KIND_OP_BWD) {
+          if (idx >= L - tail) { act = 1; slot = 2 * Tf + w.fbase[a] + ring; skey = pack_key(KIND_SYNC, a, ring, 0, 0); }
+          else {
+            int r = idx;
+            for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
+              int p = T.op_in_pairs[i];
+              int col = w.pcol[p] + c;
+              int j1 = P.col_ent_off[col], len = P.col_ent_off[col + 1] - j1;
+              if (r < len) {
+                int e = P.col_ent[j1 + r];
+                int sp = T.pair_src[p];
+                int kk = P.ent_k[e];
+                if (w.asg[T.op_slot_off[sp] + kk] == wdev) { act = 1; slot = Tf + w.fbase[sp] + kk; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); }
+                else { act = 2; skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c); saux = e; }
+                break;
+              }
+              r -= len;
+            }
+          }
+        } else if (kind == KIND_EDGE) { act = 1; slot = w.fbase[b] + d; skey = pack_key(KIND_OP, b, 0, d, 0); }
+        else if (kind == KIND_EDGE_BWD) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
+        else { act = 2; skey = pack_key(KIND_SYNC, a, b, c + 1, 0); }
       }
-      // arrivals: max(ready), then the last arriver pushes (fence pairs order the RMWs)
+      // arrivals: every max lands before any count reaches zero (syncwarp orders them)
+      if (act == 1) atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(wend));
+      __syncwarp();
       bool want = false;
       double pready = 0.0;
       if (act == 1) {
-        atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(end));
-        __threadfence_block();
-        if (atomicSub(&st.rem[slot], 1) == 1) {
-          __threadfence_block();
-          pready = *(volatile double *)&st.ready[slot];
-          want = true;
-        }
+        if (atomicSub(&st.rem[slot], 1) == 1) { pready = st.ready[slot]; want = true; }
       } else if (act == 2) {
         want = true;
-        pready = end;
+        pready = wend;
       }
       int q = 0;
       double exe = 0.0;
@@ -1109,13 +1149,14 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
       }
       unsigned bad = __ballot_sync(FULLMASK, err);
       if (bad) {
-        int srcl = __ffs(bad) - 1;
+        int s3 = __ffs(bad) - 1;
         out.status = PS_STATUS_NO_ROUTE;
-        out.err_a = __shfl_sync(FULLMASK, ea, srcl);
-        out.err_b = __shfl_sync(FULLMASK, eb, srcl);
+        out.err_a = __shfl_sync(FULLMASK, ea, s3);
+        out.err_b = __shfl_sync(FULLMASK, eb, s3);
         return out;
       }
       if (!push2(want, pready, skey, exe, q, n, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+      __syncwarp();
     }
     __syncwarp();
   }
