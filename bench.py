@@ -333,7 +333,9 @@ def run_ours(args):
                    "proposals_per_step": round(evals / args.steps, 1),
                    "rng": "philox", "l2": "flushed between steps (256 MB write)",
                    "tasks_per_eval": round(T_avg, 1), "deps_per_eval": round(E_avg, 1),
-                   "ready_capacity": info.ready_capacity, "overlap_entries": info.n_entries},
+                   "ready_capacity": info.ready_capacity, "overlap_entries": info.n_entries,
+                   "shared_counters": info.shared_counters, "resident_warps_per_sm": info.resident_warps_per_sm,
+                   "warps_per_block": info.warps_per_block},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": profiled_traffic(),
                      "note": f"B_eval = 32*T + 4*E = {bytes_per_eval:.0f} B (SURVEY 8d); peak {peak_src}"},

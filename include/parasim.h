@@ -106,6 +106,10 @@ typedef struct ps_problem_info {
   int32_t ready_capacity;
   int32_t warps_per_block;
   int64_t device_bytes; /* resident static tables */
+  int32_t shared_counters;       /* per-warp task counters kept in shared memory */
+  int32_t resident_warps_per_sm; /* candidates / chains resident per SM */
+  int32_t smem_per_block;
+  int32_t reserved_;
 } ps_problem_info;
 
 typedef struct ps_problem ps_problem;

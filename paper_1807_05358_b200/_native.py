@@ -15,7 +15,7 @@ __all__ = ["lib", "NativeUnavailable", "check", "PsProblemDesc", "PsProblemInfo"
            "PsMcmcParams", "PsChainSummary", "LIB_PATH", "ptr"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libparasim_cuda.so")
+LIB_PATH = os.environ.get("PARASIM_B200_LIB") or os.path.join(HERE, "_lib", "libparasim_cuda.so")
 
 PS_OK, PS_ERR_INVALID, PS_ERR_NO_ROUTE, PS_ERR_CYCLE, PS_ERR_CAPACITY, PS_ERR_CUDA = range(6)
 PS_STATUS_OK, PS_STATUS_NO_ROUTE, PS_STATUS_CAPACITY, PS_STATUS_STOPPED = 0, 2, 4, 9
@@ -52,7 +52,9 @@ class PsProblemDesc(ctypes.Structure):
 class PsProblemInfo(ctypes.Structure):
     _fields_ = [("n_entries", ctypes.c_int64), ("n_combos", ctypes.c_int64), ("n_queues", ctypes.c_int32),
                 ("n_slots", ctypes.c_int32), ("ready_capacity", ctypes.c_int32),
-                ("warps_per_block", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+                ("warps_per_block", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
+                ("shared_counters", ctypes.c_int32), ("resident_warps_per_sm", ctypes.c_int32),
+                ("smem_per_block", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
 
 class PsTraceTask(ctypes.Structure):

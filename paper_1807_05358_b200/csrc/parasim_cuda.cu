@@ -26,6 +26,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <stdint.h>
+#include <stdlib.h>
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -67,6 +68,7 @@ struct DevProb {
   const int *row_ent_off, *col_ent_off, *col_ent;
   const unsigned short *ent_k, *ent_l;
   const long long *ent_bytes;
+  const void *ent16, *cent16;  // packed (k | l << 16, bytes) rows and column-ordered copies
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
@@ -211,6 +213,18 @@ __global__ void k_cols(DevProb P, int n_cols, int n_combos, int *col_count, cons
     }
   }
   if (!col_off_fill) col_count[q] = cnt;
+}
+
+__global__ void k_pack(DevProb P, int n_ent, void *ent16, void *cent16) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_ent) return;
+  long long *dst = (long long *)ent16 + 2 * (size_t)e;
+  dst[0] = (long long)((unsigned)P.ent_k[e] | ((unsigned)P.ent_l[e] << 16));
+  dst[1] = P.ent_bytes[e];
+  int src = P.col_ent[e];
+  long long *cd = (long long *)cent16 + 2 * (size_t)e;
+  cd[0] = (long long)((unsigned)P.ent_k[src] | ((unsigned)P.ent_l[src] << 16));
+  cd[1] = P.ent_bytes[src];
 }
 
 // ---------------------------------------------------------------- simulator
@@ -620,9 +634,11 @@ struct Tab {  // block-shared copies of small static tables
   double *link_lat, *link_bw;
 };
 
-struct Lay {  // byte offsets / sizes shared by host and device
+struct Lay {  // sizes shared by host and device
   size_t tab_bytes, warp_bytes;
-  int S;  // dense-slot capacity of the shared-memory state
+  int SC;  // dense counter capacity (fwd + bwd + ring counters) kept in shared memory
+  int GC;  // parameter-shard (ring) capacity
+  int RC;  // staged row / column offset capacity
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -637,35 +653,37 @@ __host__ __device__ inline size_t tab_bytes_of(const DevProb &P) {
   return b;
 }
 
-__host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int S) {
+__host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC, int RC) {
   size_t b = 0;
   b += al16(4 * (size_t)P.n_ops) * 2;                // mapl, gmap
-  b += al16(4 * (size_t)(P.n_ops + 1));              // fbase
+  b += al16(4 * (size_t)(P.n_ops + 1)) * 2;          // fbase, gbase
   b += al16(4 * (size_t)P.n_pairs) * 2;              // prow, pcol
   b += al16((size_t)P.n_slots);                      // asg
   b += al16(8 * (size_t)P.n_queues) * 3;             // qclock, qready, qbest
-  b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap);  // ready set: hi, lo, exe, q
-  b += al16(8 * (size_t)3 * S) + al16(4 * (size_t)3 * S) + al16(8 * (size_t)S) + al16((size_t)S);  // state, masks, groups
-  b += al16(4 * (size_t)P.cap);                      // member list
+  b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
   b += al16(8 * (size_t)P.n_ops) * 2;                // per-op exe cache (single device kind)
-  b += 256 + 16;  // proposal staging (old assignment of the changed op)
+  b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC);  // counters: ready, remaining, shard id
+  b += al16(8 * (size_t)GC);                         // ring device masks
+  b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
+  b += 256 + 128 + 16;                               // proposal staging, phase counters
   return b;
 }
 
 struct W2 {
-  int *mapl, *gmap, *fbase, *prow, *pcol;
+  int *mapl, *gmap, *fbase, *gbase, *prow, *pcol;
   unsigned char *asg;
   double *qclock;
   unsigned long long *qready, *qbest, *rhi, *rlo;
   double *rexe;
-  int *rq;
-  double *sready;
-  int *srem;
-  unsigned long long *gmask;
-  unsigned char *sgrp;
-  int *mem;
+  int *rq, *mem;
   double *exef, *exeb;
+  double *cready;
+  unsigned short *crem;
+  unsigned char *cgrp;
+  unsigned long long *gmask;
+  int *srow, *scol;
   unsigned char *oldasg;
+  unsigned long long *ph;  // per-warp phase counters (PS_PHASES builds)
 };
 
 __device__ inline void carve_tab(char *base, const DevProb &P, Tab &t) {
@@ -706,12 +724,13 @@ __device__ inline void load_tab(const DevProb &P, const Tab &t) {
   for (int i = tid; i < P.n_links; i += nt) { t.link_lat[i] = P.link_lat[i]; t.link_bw[i] = P.link_bw[i]; }
 }
 
-__device__ inline void carve_warp(char *base, const DevProb &P, int S, W2 &w) {
+__device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2 &w) {
   char *p = base;
   auto take = [&](size_t bytes) { char *r = p; p += al16(bytes); return r; };
   w.mapl = (int *)take(4 * P.n_ops);
   w.gmap = (int *)take(4 * P.n_ops);
   w.fbase = (int *)take(4 * (P.n_ops + 1));
+  w.gbase = (int *)take(4 * (P.n_ops + 1));
   w.prow = (int *)take(4 * P.n_pairs);
   w.pcol = (int *)take(4 * P.n_pairs);
   w.asg = (unsigned char *)take(P.n_slots);
@@ -722,52 +741,31 @@ __device__ inline void carve_warp(char *base, const DevProb &P, int S, W2 &w) {
   w.rlo = (unsigned long long *)take(8 * P.cap);
   w.rexe = (double *)take(8 * P.cap);
   w.rq = (int *)take(4 * P.cap);
-  w.sready = (double *)take(8 * 3 * S);
-  w.srem = (int *)take(4 * 3 * S);
-  w.gmask = (unsigned long long *)take(8 * S);
-  w.sgrp = (unsigned char *)take(S);
   w.mem = (int *)take(4 * P.cap);
   w.exef = (double *)take(8 * P.n_ops);
   w.exeb = (double *)take(8 * P.n_ops);
+  w.cready = (double *)take(8 * L.SC);
+  w.crem = (unsigned short *)take(2 * L.SC);
+  w.cgrp = (unsigned char *)take(L.SC);
+  w.gmask = (unsigned long long *)take(8 * L.GC);
+  w.srow = (int *)take(4 * L.RC);
+  w.scol = (int *)take(4 * L.RC);
   w.oldasg = (unsigned char *)take(256);
+  w.ph = (unsigned long long *)take(128);
 }
 
-struct State {  // per-candidate dense task state (shared or global)
-  double *ready;
-  int *rem;
-  unsigned long long *gmask;
-  unsigned char *grp;  // parameter shard of each forward slot
-  int Tf;
+struct State {  // one candidate's dense counters (shared memory, or a global slice)
+  double *ready;           // [0,Tf) forward, [Tf,2Tf) backward, [2Tf,2Tf+G) ring hop 0
+  unsigned short *rem;
+  unsigned char *grp;      // parameter shard of each forward slot
+  unsigned long long *gmask;  // [G] ring devices per shard
+  const int *rowoff, *coloff;  // staged (or global) overlap row / column offsets
+  int Tf, G;
 };
 
-// exe time and queue of a task about to enter the ready set; q < 0 = no route
-__device__ __forceinline__ void task_attrs(const DevProb &P, const Tab &T, const W2 &w, const State &st,
-                                           unsigned long long key, int aux, int &q, double &exe, int &ea, int &eb) {
-  unsigned kind = key_kind(key), a = key_a(key), b = key_b(key), c = key_c(key), d = key_d(key);
-  if (kind == KIND_OP || kind == KIND_OP_BWD) {
-    int dev = w.asg[T.op_slot_off[a] + c];
-    q = dev;
-    if (P.n_kinds == 1) exe = (kind == KIND_OP ? w.exef : w.exeb)[a];
-    else exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
-    return;
-  }
-  int da, db;
-  double nb;
-  if (kind == KIND_SYNC) {
-    unsigned long long msk = st.gmask[w.fbase[a] + b];
-    int r = __popcll((long long)msk);
-    da = nth_bit(msk, c % r);
-    db = nth_bit(msk, (c + 1) % r);
-    nb = P.map_shard[w.gmap[a]] / (double)r;
-  } else {
-    da = w.asg[T.op_slot_off[a] + c];
-    db = w.asg[T.op_slot_off[b] + d];
-    nb = (double)P.ent_bytes[aux];
-  }
-  int li = T.link_of[da * P.n_dev + db];
-  if (li < 0) { q = -1; ea = da; eb = db; exe = 0.0; return; }
-  q = P.n_dev + li;
-  exe = T.link_lat[li] + nb / T.link_bw[li];
+__host__ __device__ inline size_t gscratch_bytes(int n_slots) {
+  return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 2) + al16((size_t)n_slots) +
+         al16((size_t)n_slots * 8) + 128;
 }
 
 __device__ __forceinline__ bool push2(bool want, double ready, unsigned long long key, double exe, int q, int &n,
@@ -816,101 +814,196 @@ __device__ __forceinline__ int warp_argmin128(unsigned long long hi, unsigned lo
 
 __device__ __forceinline__ unsigned long long warp_min64(unsigned long long x, int lane) {
   unsigned v = (unsigned)(x >> 32), mn = __reduce_min_sync(FULLMASK, v);
-  bool c = v == mn;
-  unsigned lo = c ? (unsigned)x : 0xffffffffu;
+  unsigned lo = v == mn ? (unsigned)x : 0xffffffffu;
   unsigned mlo = __reduce_min_sync(FULLMASK, lo);
   return ((unsigned long long)mn << 32) | mlo;
 }
 
-// Candidate setup: gmap, dense bases, per-pair combo bases, state placement.
-__device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2 &w, int S, char *gscratch, int lane) {
-  // gmap + dense prefix of map sizes
-  int carry = 0;
+// Candidate setup: maps, dense bases, staged overlap offsets, state placement.
+__device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch,
+                                        int lane) {
+  int carry = 0, gcarry = 0;
   for (int base = 0; base < P.n_ops; base += 32) {
     int o = base + lane;
-    int sz = 0;
+    int sz = 0, ng = 0;
     if (o < P.n_ops) {
       int g = T.op_map_off[o] + w.mapl[o];
       w.gmap[o] = g;
       sz = P.map_size[g];
+      ng = T.op_param_mask[o] >= 0 ? P.map_ngroups[g] : 0;
       if (P.n_kinds == 1) { w.exef[o] = P.exe_fwd[g]; w.exeb[o] = P.exe_bwd[g]; }
     }
-    int incl = sz;
+    int a = sz, b = ng;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      int y = __shfl_up_sync(FULLMASK, incl, off);
-      if (lane >= off) incl += y;
+      int ya = __shfl_up_sync(FULLMASK, a, off), yb = __shfl_up_sync(FULLMASK, b, off);
+      if (lane >= off) { a += ya; b += yb; }
     }
-    if (o < P.n_ops) w.fbase[o] = carry + incl - sz;
-    carry += __shfl_sync(FULLMASK, incl, 31);
+    if (o < P.n_ops) { w.fbase[o] = carry + a - sz; w.gbase[o] = gcarry + b - ng; }
+    carry += __shfl_sync(FULLMASK, a, 31);
+    gcarry += __shfl_sync(FULLMASK, b, 31);
   }
-  if (lane == 0) w.fbase[P.n_ops] = carry;
+  if (lane == 0) { w.fbase[P.n_ops] = carry; w.gbase[P.n_ops] = gcarry; }
+  // per pair: global row/col base of the current combo and the staged layout
+  int rcarry = 0, ccarry = 0;
+  for (int base = 0; base < P.n_pairs; base += 32) {
+    int p = base + lane;
+    int nr = 0, nc = 0;
+    if (p < P.n_pairs) {
+      int s = T.pair_src[p], d = T.pair_dst[p];
+      nr = P.map_size[w.gmap[s]] + 1;
+      nc = P.full ? P.map_size[w.gmap[d]] + 1 : 0;
+    }
+    int a = nr, b = nc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int ya = __shfl_up_sync(FULLMASK, a, off), yb = __shfl_up_sync(FULLMASK, b, off);
+      if (lane >= off) { a += ya; b += yb; }
+    }
+    if (p < P.n_pairs) {
+      w.prow[p] = rcarry + a - nr;  // staged base (replaced by the global row if not staged)
+      w.pcol[p] = ccarry + b - nc;
+    }
+    rcarry += __shfl_sync(FULLMASK, a, 31);
+    ccarry += __shfl_sync(FULLMASK, b, 31);
+  }
+  __syncwarp();
+  bool stage_r = rcarry <= L.RC, stage_c = ccarry <= L.RC;
   for (int p = lane; p < P.n_pairs; p += 32) {
     int s = T.pair_src[p], d = T.pair_dst[p];
     int nmd = T.op_map_off[d + 1] - T.op_map_off[d];
     int cc = T.combo_off[p] + w.mapl[s] * nmd + w.mapl[d];
-    w.prow[p] = P.combo_row_off[cc];
-    w.pcol[p] = P.combo_col_off[cc];
+    int grow = P.combo_row_off[cc], gcol = P.combo_col_off[cc];
+    int nr = P.map_size[w.gmap[s]] + 1, nc = P.map_size[w.gmap[d]] + 1;
+    if (stage_r) {
+      int dst = w.prow[p];
+      for (int k = 0; k < nr; ++k) w.srow[dst + k] = P.row_ent_off[grow + k];
+    } else {
+      w.prow[p] = grow;
+    }
+    if (P.full) {
+      if (stage_c) {
+        int dst = w.pcol[p];
+        for (int k = 0; k < nc; ++k) w.scol[dst + k] = P.col_ent_off[gcol + k];
+      } else {
+        w.pcol[p] = gcol;
+      }
+    }
   }
   State st;
   st.Tf = carry;
-  if (carry <= S) {
-    st.ready = w.sready; st.rem = w.srem; st.gmask = w.gmask; st.grp = w.sgrp;
+  st.G = gcarry;
+  st.rowoff = stage_r ? w.srow : P.row_ent_off;
+  st.coloff = stage_c ? w.scol : P.col_ent_off;
+  int need = P.full ? 2 * carry + gcarry : carry;
+  if (need <= L.SC && gcarry <= L.GC) {
+    st.ready = w.cready; st.rem = w.crem; st.grp = w.cgrp; st.gmask = w.gmask;
   } else {
-    st.ready = (double *)gscratch;
-    st.rem = (int *)(st.ready + 3 * (size_t)P.n_slots);
-    st.gmask = (unsigned long long *)(st.rem + 3 * (size_t)P.n_slots + 2);
-    st.gmask = (unsigned long long *)(((size_t)st.gmask + 15) & ~(size_t)15);
-    st.grp = (unsigned char *)(st.gmask + P.n_slots);
+    char *g = gscratch;
+    st.ready = (double *)g; g += al16((size_t)P.n_slots * 3 * 8);
+    st.rem = (unsigned short *)g; g += al16((size_t)P.n_slots * 3 * 2);
+    st.grp = (unsigned char *)g; g += al16((size_t)P.n_slots);
+    st.gmask = (unsigned long long *)g;
   }
   __syncwarp();
   return st;
 }
 
-__host__ __device__ inline size_t gscratch_bytes(int n_slots) {
-  return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 4 + 16) + al16((size_t)n_slots * 8) +
-         al16((size_t)n_slots) + 128;
+// exe time / queue of a transfer between devices da -> db carrying nb bytes
+__device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int da, int db, double nb, int &q,
+                                           double &exe) {
+  int li = T.link_of[da * P.n_dev + db];
+  if (li < 0) return false;
+  q = P.n_dev + li;
+  exe = T.link_lat[li] + nb / T.link_bw[li];
+  return true;
 }
 
-__device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, int S, char *gscratch, int lane) {
+__device__ __forceinline__ void op_attrs(const DevProb &P, const Tab &T, const W2 &w, unsigned kind, int a, int c,
+                                         int &q, double &exe) {
+  int dev = w.asg[T.op_slot_off[a] + c];
+  q = dev;
+  if (P.n_kinds == 1) exe = (kind == KIND_OP ? w.exef : w.exeb)[a];
+  else exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
+}
+
+__device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const W2 &w, const State &st, int a, int si,
+                                           int hop, int &q, double &exe, int &ea, int &eb) {
+  unsigned long long msk = st.gmask[w.gbase[a] + si];
+  int r = __popcll((long long)msk);
+  int da = nth_bit(msk, hop % r), db = nth_bit(msk, (hop + 1) % r);
+  if (!link_attrs(P, T, da, db, P.map_shard[w.gmap[a]] / (double)r, q, exe)) { ea = da; eb = db; return false; }
+  return true;
+}
+
+struct Ent16 { int kl; int pad; long long bytes; };  // k | l << 16, transfer bytes
+
+#ifdef PS_PHASES
+__device__ unsigned long long g_phase[16];
+#define PH_T(v) long long v = clock64()
+#define PH_ADD(i, t0) do { if (lane == 0) w.ph[i] += (unsigned long long)(clock64() - (t0)); } while (0)
+#define PH_CNT(i, x) do { if (lane == 0) w.ph[i] += (unsigned long long)(x); } while (0)
+#else
+#define PH_T(v)
+#define PH_ADD(i, t0)
+#define PH_CNT(i, x)
+#endif
+
+__device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   SimOut out;
   out.makespan = 0.0;
   out.status = PS_STATUS_OK;
   out.err_a = out.err_b = -1;
-  State st = setup_candidate(P, T, w, S, gscratch, lane);
+  PH_T(t_setup);
+  State st = setup_candidate(P, T, w, L, gscratch, lane);
+  PH_ADD(0, t_setup);
+  PH_CNT(8, 1);
+  PH_CNT(9, st.rowoff == w.srow ? 1 : 0);
   const int Tf = st.Tf;
+  PH_CNT(10, (P.full ? 2 * Tf + st.G : Tf) <= L.SC ? 1 : 0);
+  const Ent16 *ent = (const Ent16 *)P.ent16;
+  const Ent16 *cent = (const Ent16 *)P.cent16;
   for (int q = lane; q < P.n_queues; q += 32) { w.qclock[q] = 0.0; w.qready[q] = ~0ull; w.qbest[q] = ~0ull; }
   if (P.full)
-    for (int s = lane; s < Tf; s += 32) st.gmask[s] = 0ull;
+    for (int s = lane; s < st.G; s += 32) st.gmask[s] = 0ull;
   __syncwarp();
-  // ---- init: in-degrees, ring membership, sources
+  // ---- init: in-degrees, ring membership
+  PH_T(t_init);
   for (int s = lane; s < Tf; s += 32) {
     int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
     int k = s - w.fbase[o];
     int indeg = 0;
     for (int i = T.op_in_off[o]; i < T.op_in_off[o + 1]; ++i) {
       int col = w.pcol[T.op_in_pairs[i]] + k;
-      indeg += P.col_ent_off[col + 1] - P.col_ent_off[col];
+      if (P.full) indeg += st.coloff[col + 1] - st.coloff[col];
+      else {  // forward mode: columns are not staged; count from the global index
+        int p = T.op_in_pairs[i];
+        int sp = T.pair_src[p];
+        int nmd = T.op_map_off[o + 1] - T.op_map_off[o];
+        int gc = P.combo_col_off[T.combo_off[p] + w.mapl[sp] * nmd + w.mapl[o]] + k;
+        indeg += P.col_ent_off[gc + 1] - P.col_ent_off[gc];
+      }
     }
-    st.rem[s] = indeg;
+    st.rem[s] = (unsigned short)indeg;
     st.ready[s] = 0.0;
     if (P.full) {
       int outd = 1;
       for (int i = T.op_out_off[o]; i < T.op_out_off[o + 1]; ++i) {
         int row = w.prow[T.op_out_pairs[i]] + k;
-        outd += P.row_ent_off[row + 1] - P.row_ent_off[row];
+        outd += st.rowoff[row + 1] - st.rowoff[row];
       }
-      st.rem[Tf + s] = outd;
+      st.rem[Tf + s] = (unsigned short)outd;
       st.ready[Tf + s] = 0.0;
       int pm = T.op_param_mask[o];
       if (pm >= 0) {
         int g = w.gmap[o];
         int si = group_of2(P, o, g, k, pm);
         st.grp[s] = (unsigned char)si;
-        atomicOr(&st.gmask[w.fbase[o] + si], 1ull << w.asg[T.op_slot_off[o] + k]);
+        atomicOr(&st.gmask[w.gbase[o] + si], 1ull << w.asg[T.op_slot_off[o] + k]);
         if (k < P.map_ngroups[g]) {
-          st.rem[2 * Tf + s] = P.map_size[g] / P.map_ngroups[g];
-          st.ready[2 * Tf + s] = 0.0;
+          int c = 2 * Tf + w.gbase[o] + k;
+          st.rem[c] = (unsigned short)(P.map_size[g] / P.map_ngroups[g]);
+          st.ready[c] = 0.0;
         }
       }
     }
@@ -927,110 +1020,155 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
     if (s < Tf && st.rem[s] == 0) {
       int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
       key = pack_key(KIND_OP, o, 0, s - w.fbase[o], 0);
-      int ea, eb;
-      task_attrs(P, T, w, st, key, 0, q, exe, ea, eb);
+      op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe);
       want = true;
     }
     okc &= push2(want, 0.0, key, exe, q, n, P, w, lane);
   }
   __syncwarp();
+  PH_ADD(1, t_init);
   if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
-
   while (n > 0) {
-    // ---- scan 1: minimum key and LB = min(ready + exe)
-    unsigned long long bh = ~0ull, bl = ~0ull, lb = ~0ull;
-    for (int i = lane; i < n; i += 32) {
-      unsigned long long h = w.rhi[i], l = w.rlo[i];
-      if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; }
-      double e = __longlong_as_double((long long)h) + w.rexe[i];
-      unsigned long long eb = (unsigned long long)__double_as_longlong(e);
-      if (eb < lb) lb = eb;
-    }
-    int wl = warp_argmin128(bh, bl, lane);
-    unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
-    double LB = __longlong_as_double((long long)warp_min64(lb, lane));
-    // ---- scan 2: members (ready < LB, or the global minimum) -> member list,
-    // and each bids its ready time for its queue
-    int nm = 0;
-    for (int base = 0; base < n; base += 32) {
-      int i = base + lane;
-      bool mem = false;
-      if (i < n) {
-        unsigned long long h2 = w.rhi[i];
-        mem = __longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey;
-        if (mem) atomicMin(&w.qready[w.rq[i]], h2);
-      }
-      unsigned bm = __ballot_sync(FULLMASK, mem);
-      if (mem) w.mem[nm + __popc(bm & ((1u << lane) - 1u))] = i;
-      nm += __popc(bm);
-    }
-    __syncwarp();
-    // ---- members tied on their queue's ready time bid their origin key
-    for (int j = lane; j < nm; j += 32) {
-      int i = w.mem[j];
-      int q2 = w.rq[i];
-      if (w.qready[q2] == w.rhi[i]) atomicMin(&w.qbest[q2], w.rlo[i]);
-    }
-    __syncwarp();
-    // ---- winners: each queue's minimum (ready, origin); lane k holds winner k
+    PH_T(t_sel);
+    PH_CNT(11, 1);
+    PH_CNT(12, n);
     int nw = 0;
     unsigned long long mykey = 0;
     double myready = 0.0, myexe = 0.0;
-    int myq = -1, mypos = -1;
-    for (int base = 0; base < nm && nw < 32; base += 32) {
-      int j = base + lane;
-      bool win = false;
-      int i = 0;
-      if (j < nm) {
-        i = w.mem[j];
+    int myq = -1;
+    if (n <= 32) {
+      // ---- fast path: entry `lane` lives in this lane's registers for the round
+      bool valid = lane < n;
+      unsigned long long h = valid ? w.rhi[lane] : ~0ull, k = valid ? w.rlo[lane] : ~0ull;
+      double e = valid ? w.rexe[lane] : 0.0;
+      int q = valid ? w.rq[lane] : 0;
+      double r = __longlong_as_double((long long)h);
+      unsigned long long lbb = valid ? (unsigned long long)__double_as_longlong(r + e) : ~0ull;
+      double LB = __longlong_as_double((long long)warp_min64(lbb, lane));
+      bool member = valid && r < LB;
+      if (!__any_sync(FULLMASK, member)) {
+        // degenerate (zero or absorbed exe): the global minimum alone
+        int wl = warp_argmin128(h, k, lane);
+        member = lane == wl;
+      }
+      // per-queue minimum (ready, origin) among members: a member alone on its
+      // queue wins outright; ties on a queue take a group-restricted lexicographic min
+      unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
+      bool win = member;
+      if (member && __popc(gm) > 1) {
+        unsigned cand = gm, v, mn;
+        v = (unsigned)(h >> 32); mn = __reduce_min_sync(gm, v); cand &= __ballot_sync(gm, v == mn);
+        v = (cand >> lane & 1) ? (unsigned)h : 0xffffffffu; mn = __reduce_min_sync(gm, v);
+        cand &= __ballot_sync(gm, v == mn);
+        v = (cand >> lane & 1) ? (unsigned)(k >> 32) : 0xffffffffu; mn = __reduce_min_sync(gm, v);
+        cand &= __ballot_sync(gm, v == mn);
+        v = (cand >> lane & 1) ? (unsigned)k : 0xffffffffu; mn = __reduce_min_sync(gm, v);
+        cand &= __ballot_sync(gm, v == mn);
+        win = (__ffs(cand) - 1) == lane;
+      }
+      unsigned wb = __ballot_sync(FULLMASK, win);
+      nw = __popc(wb);
+      if (win) { w.qbest[q] = ~0ull; w.qready[q] = ~0ull; }  // clears a bid left by an earlier capped round
+      bool keep = valid && !win;
+      unsigned kb = __ballot_sync(FULLMASK, keep);
+      __syncwarp();
+      if (keep) {
+        int pos = __popc(kb & ((1u << lane) - 1u));
+        w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = q;
+      }
+      n = __popc(kb);
+      int src = lane < nw ? (int)__fns(wb, 0, lane + 1) : 0;
+      mykey = __shfl_sync(FULLMASK, k, src);
+      myready = __shfl_sync(FULLMASK, r, src);
+      myexe = __shfl_sync(FULLMASK, e, src);
+      myq = __shfl_sync(FULLMASK, q, src);
+      __syncwarp();
+    } else {
+      // ---- scan 1: minimum key and LB = min(ready + exe)
+      unsigned long long bh = ~0ull, bl = ~0ull, lb = ~0ull;
+      for (int i = lane; i < n; i += 32) {
+        unsigned long long h = w.rhi[i], l = w.rlo[i];
+        if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; }
+        double e = __longlong_as_double((long long)h) + w.rexe[i];
+        unsigned long long eb = (unsigned long long)__double_as_longlong(e);
+        if (eb < lb) lb = eb;
+      }
+      int wl = warp_argmin128(bh, bl, lane);
+      unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
+      double LB = __longlong_as_double((long long)warp_min64(lb, lane));
+      // ---- scan 2: members (ready < LB, or the global minimum) -> member list,
+      // and each bids its ready time for its queue
+      int nm = 0;
+      for (int base = 0; base < n; base += 32) {
+        int i = base + lane;
+        bool mem = false;
+        if (i < n) {
+          unsigned long long h2 = w.rhi[i];
+          mem = __longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey;
+          if (mem) atomicMin(&w.qready[w.rq[i]], h2);
+        }
+        unsigned bm = __ballot_sync(FULLMASK, mem);
+        if (mem) w.mem[nm + __popc(bm & ((1u << lane) - 1u))] = i;
+        nm += __popc(bm);
+      }
+      __syncwarp();
+      // ---- members tied on their queue's ready time bid their origin key
+      for (int j = lane; j < nm; j += 32) {
+        int i = w.mem[j];
         int q2 = w.rq[i];
-        win = w.qbest[q2] == w.rlo[i] && w.qready[q2] == w.rhi[i];
+        if (w.qready[q2] == w.rhi[i]) atomicMin(&w.qbest[q2], w.rlo[i]);
       }
-      unsigned bm = __ballot_sync(FULLMASK, win);
-      int rank = __popc(bm & ((1u << lane) - 1u));
-      int slot = nw + rank;
-      // winner at member position -> lane `slot` (ignored beyond 32)
-      for (int src = 0; src < 32; ++src) {
-        if (!(bm >> src & 1)) continue;
-        int s2 = __shfl_sync(FULLMASK, slot, src);
+      __syncwarp();
+      // ---- winners: each queue's minimum (ready, origin); lane k holds winner k
+      int mypos = -1;
+      for (int base = 0; base < nm && nw < 32; base += 32) {
+        int j = base + lane;
+        bool win = false;
+        int i = 0;
+        if (j < nm) {
+          i = w.mem[j];
+          int q2 = w.rq[i];
+          win = w.qbest[q2] == w.rlo[i] && w.qready[q2] == w.rhi[i];
+        }
+        unsigned bm = __ballot_sync(FULLMASK, win);
+        // lane nw + r takes the r-th winner of this chunk (winners past 32 wait)
+        int r = lane - nw;
+        int src = (r >= 0 && r < __popc(bm)) ? (int)__fns(bm, 0, r + 1) : 0;
         int i2 = __shfl_sync(FULLMASK, i, src);
-        if (lane == s2 && s2 < 32) mypos = i2;
+        if (r >= 0 && r < __popc(bm)) mypos = i2;
+        nw = min(32, nw + __popc(bm));
       }
-      nw = min(32, nw + __popc(bm));
+      bool mine0 = lane < nw;
+      if (mine0) {
+        mykey = w.rlo[mypos];
+        myready = __longlong_as_double((long long)w.rhi[mypos]);
+        myexe = w.rexe[mypos];
+        myq = w.rq[mypos];
+      }
+      __syncwarp();
+      if (mine0) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rhi[mypos] = ~0ull; }
+      __syncwarp();
+      // ---- remove the winners: refill holes below n-nw with survivors from the tail
+      {
+        int tailpos = n - nw + lane;
+        bool survivor = lane < nw && w.rhi[tailpos] != ~0ull;
+        unsigned sm = __ballot_sync(FULLMASK, survivor);
+        bool head_hole = mine0 && mypos < n - nw;
+        unsigned hm = __ballot_sync(FULLMASK, head_hole);
+        int hrank = __popc(hm & ((1u << lane) - 1u));
+        int src = -1;
+        if (head_hole) src = n - nw + (int)__fns(sm, 0, hrank + 1);
+        unsigned long long h2 = 0, k2 = 0;
+        double e2 = 0.0;
+        int q2 = 0;
+        if (head_hole) { h2 = w.rhi[src]; k2 = w.rlo[src]; e2 = w.rexe[src]; q2 = w.rq[src]; }
+        __syncwarp();
+        if (head_hole) { w.rhi[mypos] = h2; w.rlo[mypos] = k2; w.rexe[mypos] = e2; w.rq[mypos] = q2; }
+        n -= nw;
+        __syncwarp();
+      }
     }
     bool mine = lane < nw;
-    if (mine) {
-      mykey = w.rlo[mypos];
-      myready = __longlong_as_double((long long)w.rhi[mypos]);
-      myexe = w.rexe[mypos];
-      myq = w.rq[mypos];
-    }
-    __syncwarp();
-    if (mine) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rhi[mypos] = ~0ull; }
-    __syncwarp();
-    // ---- remove the winners: refill holes below n-nw with survivors from the tail
-    {
-      int tailpos = n - nw + lane;
-      bool survivor = lane < nw && w.rhi[tailpos] != ~0ull;
-      unsigned sm = __ballot_sync(FULLMASK, survivor);
-      bool head_hole = mine && mypos < n - nw;
-      unsigned hm = __ballot_sync(FULLMASK, head_hole);
-      int hrank = __popc(hm & ((1u << lane) - 1u));
-      int src = -1;
-      if (head_hole) {
-        unsigned x = sm;
-        for (int r = 0; r < hrank; ++r) x &= x - 1;
-        src = n - nw + __ffs(x) - 1;
-      }
-      unsigned long long h2 = 0, k2 = 0;
-      double e2 = 0.0;
-      int q2 = 0;
-      if (head_hole) { h2 = w.rhi[src]; k2 = w.rlo[src]; e2 = w.rexe[src]; q2 = w.rq[src]; }
-      __syncwarp();
-      if (head_hole) { w.rhi[mypos] = h2; w.rlo[mypos] = k2; w.rexe[mypos] = e2; w.rq[mypos] = q2; }
-      n -= nw;
-      __syncwarp();
-    }
     // ---- run the winners: distinct queues, each its queue's next task
     double end = 0.0;
     if (mine) {
@@ -1040,112 +1178,172 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
       w.qclock[myq] = end;
       if (end > out.makespan) out.makespan = end;
     }
+    PH_ADD(2, t_sel);
+    PH_CNT(13, nw);
+    PH_T(t_succ);
     // ---- successors: lane groups of G per winner, random access into each list
-    int lg = 31 - __clz(nw);           // floor(log2 nw)
-    if ((1 << lg) < nw) ++lg;          // ceil
-    int G = 32 >> lg;
-    int wi = lane / G, j0 = lane % G;
+    int lg = 31 - __clz(nw);
+    if ((1 << lg) < nw) ++lg;
+    int G = 32 >> lg, lgG = 5 - lg;
+    int wi = lane >> lgG, j0 = lane & (G - 1);
     bool act_lane = wi < nw;
     int srcl = act_lane ? wi : 0;
     unsigned long long wkey = __shfl_sync(FULLMASK, mykey, srcl);
     double wend = __shfl_sync(FULLMASK, end, srcl);
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
     int wdev = 0, head = 0, tail = 0, L = 0, ring = 0;
+    int fe = -1, fp = 0;  // this lane's first list entry (index j0) and its pair
+    Ent16 fen;
+    fen.kl = 0; fen.pad = 0; fen.bytes = 0;
     if (act_lane) {
       if (kind == KIND_OP || kind == KIND_OP_BWD) wdev = w.asg[T.op_slot_off[a] + c];
       if (kind == KIND_OP) {
         head = P.full ? 1 : 0;
         L = head;
+        int r0 = j0 - head;
         for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
-          int row = w.prow[T.op_out_pairs[i]] + c;
-          L += P.row_ent_off[row + 1] - P.row_ent_off[row];
+          int p = T.op_out_pairs[i];
+          int row = w.prow[p] + c;
+          int e0 = st.rowoff[row], len = st.rowoff[row + 1] - e0;
+          if (fe < 0 && r0 >= 0 && r0 < len) { fe = e0 + r0; fp = p; }
+          r0 -= len;
+          L += len;
         }
+        if (fe >= 0) fen = ent[fe];
       } else if (kind == KIND_OP_BWD) {
+        int r0 = j0;
         for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
-          int col = w.pcol[T.op_in_pairs[i]] + c;
-          L += P.col_ent_off[col + 1] - P.col_ent_off[col];
+          int p = T.op_in_pairs[i];
+          int col = w.pcol[p] + c;
+          int j1 = st.coloff[col], len = st.coloff[col + 1] - j1;
+          if (fe < 0 && r0 >= 0 && r0 < len) { fe = j1 + r0; fp = p; }
+          r0 -= len;
+          L += len;
         }
+        if (fe >= 0) fen = cent[fe];
         if (T.op_param_mask[a] >= 0) {
-          int s0 = w.fbase[a] + c;
-          int si = st.grp[s0];
-          if (__popcll((long long)st.gmask[w.fbase[a] + si]) >= 2) { tail = 1; ring = si; }
+          int si = st.grp[w.fbase[a] + c];
+          if (__popcll((long long)st.gmask[w.gbase[a] + si]) >= 2) { tail = 1; ring = si; }
         }
         L += tail;
       } else if (kind == KIND_SYNC) {
-        int r = __popcll((long long)st.gmask[w.fbase[a] + b]);
+        int r = __popcll((long long)st.gmask[w.gbase[a] + b]);
         L = ((int)c + 1 < 2 * (r - 1)) ? 1 : 0;
       } else {
         L = 1;
       }
     }
-    int iters = (L + G - 1) / G;
+    int iters = (L + G - 1) >> lgG;
     iters = (int)__reduce_max_sync(FULLMASK, (unsigned)(act_lane ? iters : 0));
-    bool err = false;
-    int ea = -1, eb = -1;
+    PH_ADD(3, t_succ);
+    PH_CNT(14, iters);
+    PH_T(t_it);
     for (int t = 0; t < iters; ++t) {
       int idx = j0 + t * G;
-      int act = 0;  // 1 arrive, 2 push
-      int slot = 0, saux = 0;
+      int act = 0;  // 1 arrive at counter `slot`, 2 push task `skey` directly
+      int slot = 0;
       unsigned long long skey = 0;
+      int pq = 0;
+      double pexe = 0.0;
+      bool err = false;
+      int ea = -1, eb = -1;
       if (act_lane && idx < L) {
         if (kind == KIND_OP) {
           if (idx < head) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
           else {
             int r = idx - head;
-            for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
-              int p = T.op_out_pairs[i];
-              int row = w.prow[p] + c;
-              int e0 = P.row_ent_off[row], len = P.row_ent_off[row + 1] - e0;
-              if (r < len) {
-                int e = e0 + r;
-                int dp = T.pair_dst[p];
-                int l = P.ent_l[e];
-                if (w.asg[T.op_slot_off[dp] + l] == wdev) { act = 1; slot = w.fbase[dp] + l; skey = pack_key(KIND_OP, dp, 0, l, 0); }
-                else { act = 2; skey = pack_key(KIND_EDGE, a, dp, c, l); saux = e; }
-                break;
+            Ent16 en = fen;
+            int p = fp;
+            if (t > 0) {
+              for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
+                p = T.op_out_pairs[i];
+                int row = w.prow[p] + c;
+                int e0 = st.rowoff[row], len = st.rowoff[row + 1] - e0;
+                if (r < len) { en = ent[e0 + r]; break; }
+                r -= len;
               }
-              r -= len;
+            }
+            {
+              {
+                int dp = T.pair_dst[p];
+                int l = en.kl >> 16;
+                int ddev = w.asg[T.op_slot_off[dp] + l];
+                if (ddev == wdev) { act = 1; slot = w.fbase[dp] + l; skey = pack_key(KIND_OP, dp, 0, l, 0); }
+                else {
+                  act = 2;
+                  skey = pack_key(KIND_EDGE, a, dp, c, l);
+                  if (!link_attrs(P, T, wdev, ddev, (double)en.bytes, pq, pexe)) { err = true; ea = wdev; eb = ddev; }
+                }
+              }
             }
           }
         } else if (kind == KIND_OP_BWD) {
-          if (idx >= L - tail) { act = 1; slot = 2 * Tf + w.fbase[a] + ring; skey = pack_key(KIND_SYNC, a, ring, 0, 0); }
+          if (idx >= L - tail) { act = 1; slot = 2 * Tf + w.gbase[a] + ring; skey = pack_key(KIND_SYNC, a, ring, 0, 0); }
           else {
             int r = idx;
-            for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
-              int p = T.op_in_pairs[i];
-              int col = w.pcol[p] + c;
-              int j1 = P.col_ent_off[col], len = P.col_ent_off[col + 1] - j1;
-              if (r < len) {
-                int e = P.col_ent[j1 + r];
-                int sp = T.pair_src[p];
-                int kk = P.ent_k[e];
-                if (w.asg[T.op_slot_off[sp] + kk] == wdev) { act = 1; slot = Tf + w.fbase[sp] + kk; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); }
-                else { act = 2; skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c); saux = e; }
-                break;
+            Ent16 en = fen;
+            int p = fp;
+            if (t > 0) {
+              for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
+                p = T.op_in_pairs[i];
+                int col = w.pcol[p] + c;
+                int j1 = st.coloff[col], len = st.coloff[col + 1] - j1;
+                if (r < len) { en = cent[j1 + r]; break; }
+                r -= len;
               }
-              r -= len;
+            }
+            {
+              {
+                int sp = T.pair_src[p];
+                int kk = en.kl & 0xffff;
+                int sdev = w.asg[T.op_slot_off[sp] + kk];
+                if (sdev == wdev) { act = 1; slot = Tf + w.fbase[sp] + kk; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); }
+                else {
+                  act = 2;
+                  skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c);
+                  if (!link_attrs(P, T, sdev, wdev, (double)en.bytes, pq, pexe)) { err = true; ea = sdev; eb = wdev; }
+                }
+              }
             }
           }
         } else if (kind == KIND_EDGE) { act = 1; slot = w.fbase[b] + d; skey = pack_key(KIND_OP, b, 0, d, 0); }
         else if (kind == KIND_EDGE_BWD) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
-        else { act = 2; skey = pack_key(KIND_SYNC, a, b, c + 1, 0); }
+        else {
+          act = 2;
+          skey = pack_key(KIND_SYNC, a, b, c + 1, 0);
+          if (!sync_attrs(P, T, w, st, a, b, c + 1, pq, pexe, ea, eb)) err = true;
+        }
       }
-      // arrivals: every max lands before any count reaches zero (syncwarp orders them)
-      if (act == 1) atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(wend));
-      __syncwarp();
+      // arrivals at the same counter in this iteration merge into one update by
+      // the group's lowest lane (max of the ends, count of arrivals): no atomics
+      unsigned gm = __match_any_sync(FULLMASK, act == 1 ? slot : (0x40000000 | lane));
       bool want = false;
       double pready = 0.0;
       if (act == 1) {
-        if (atomicSub(&st.rem[slot], 1) == 1) { pready = st.ready[slot]; want = true; }
+        double gmax = wend;
+        if (__popc(gm) > 1) {
+          unsigned long long eb64 = (unsigned long long)__double_as_longlong(wend);
+          unsigned hi = __reduce_max_sync(gm, (unsigned)(eb64 >> 32));
+          unsigned lo = __reduce_max_sync(gm, (unsigned)(eb64 >> 32) == hi ? (unsigned)eb64 : 0u);
+          gmax = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+        }
+        if (lane == __ffs(gm) - 1) {
+          double rr = st.ready[slot];
+          if (gmax > rr) { rr = gmax; st.ready[slot] = rr; }
+          int left = (int)st.rem[slot] - __popc(gm);
+          st.rem[slot] = (unsigned short)left;
+          if (left == 0) {
+            want = true;
+            pready = rr;
+            unsigned sk = key_kind(skey);
+            op_attrs(P, T, w, sk == KIND_SYNC ? KIND_OP : sk, key_a(skey), key_c(skey), pq, pexe);
+            if (sk == KIND_SYNC && !sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb))
+              err = true;
+          }
+        }
       } else if (act == 2) {
         want = true;
         pready = wend;
-      }
-      int q = 0;
-      double exe = 0.0;
-      if (want) {
-        task_attrs(P, T, w, st, skey, saux, q, exe, ea, eb);
-        if (q < 0) { err = true; want = false; }
       }
       unsigned bad = __ballot_sync(FULLMASK, err);
       if (bad) {
@@ -1155,9 +1353,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
         out.err_b = __shfl_sync(FULLMASK, eb, s3);
         return out;
       }
-      if (!push2(want, pready, skey, exe, q, n, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+      if (!push2(want, pready, skey, pexe, pq, n, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
       __syncwarp();
     }
+    PH_ADD(4, t_it);
     __syncwarp();
   }
   // makespan: max over lanes
@@ -1167,8 +1366,6 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, in
   out.makespan = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
   return out;
 }
-
-
 
 __global__ void __launch_bounds__(128)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
@@ -1180,7 +1377,7 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
   __syncthreads();
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   W2 w;
-  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay.S, w);
+  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay, w);
   int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
   char *gs = gscratch + (size_t)gw * gscratch_bytes(P.n_slots);
   for (int cand = gw; cand < n; cand += nw) {
@@ -1189,7 +1386,7 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
     for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = m[i];
     for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = a[i];
     __syncwarp();
-    SimOut o = warp_simulate2(P, T, w, lay.S, gs, lane);
+    SimOut o = warp_simulate2(P, T, w, lay, gs, lane);
     if (lane == 0) {
       makespan[cand] = o.status == PS_STATUS_OK ? o.makespan : -1.0;
       status[cand] = o.status;
@@ -1382,7 +1579,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   int chain = blockIdx.x * wpb + wib;
   if (chain >= n_chains) return;
   W2 w;
-  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay.S, w);
+  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay, w);
   char *gs = gscratch + (size_t)chain * gscratch_bytes(P.n_slots);
   int *gmapl = maps + (size_t)chain * P.n_ops;
   unsigned char *gasg = asgs + (size_t)chain * P.n_slots;
@@ -1403,7 +1600,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   int *bmap = best_maps + (size_t)chain * P.n_ops;
   unsigned char *basg = best_asgs + (size_t)chain * P.n_slots;
   if (!cs.started) {
-    SimOut o = warp_simulate2(P, T, w, lay.S, gs, lane);
+    SimOut o = warp_simulate2(P, T, w, lay, gs, lane);
     cs.started = 1;
     if (o.status != PS_STATUS_OK) {
       cs.status = o.status; cs.err_a = o.err_a; cs.err_b = o.err_b;
@@ -1417,7 +1614,14 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     for (int i = lane; i < P.n_slots; i += 32) basg[i] = w.asg[i];
   }
   unsigned long long t0 = globaltimer_ns();
+#ifdef PS_PHASES
+  for (int i = lane; i < 16; i += 32) w.ph[i] = 0;
+  __syncwarp();
+#endif
+  PH_T(t_loop);
+  int n_it = 0;
   for (int it = 0; it < proposals; ++it) {
+    ++n_it;
     if (budget_ns) {  // time-boxed segment: stop between proposals once the budget is spent
       unsigned long long now = __shfl_sync(FULLMASK, globaltimer_ns(), 0);
       if (now - t0 >= budget_ns) break;
@@ -1446,7 +1650,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     if (same) {
       cand = cs.cost;
     } else {
-      SimOut so = warp_simulate2(P, T, w, lay.S, gs, lane);
+      SimOut so = warp_simulate2(P, T, w, lay, gs, lane);
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
         break;
@@ -1478,6 +1682,12 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     }
     __syncwarp();
   }
+  PH_ADD(6, t_loop);
+  PH_CNT(7, n_it);
+#ifdef PS_PHASES
+  __syncwarp();
+  if (lane < 16) atomicAdd(&g_phase[lane], w.ph[lane]);
+#endif
   for (int i = lane; i < P.n_ops; i += 32) gmapl[i] = w.mapl[i];
   for (int i = lane; i < P.n_slots; i += 32) gasg[i] = w.asg[i];
   cs.key = rng.key;
@@ -1669,6 +1879,13 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   P.col_ent_off = coff;
   if (n_cols) k_cols<<<(n_cols + 127) / 128, 128>>>(P, n_cols, n_combos, nullptr, coff);
   CK(cudaGetLastError());
+  void *e16 = nullptr, *c16 = nullptr;
+  CK(cudaMalloc(&e16, (size_t)(n_ent + 1) * 16));
+  CK(cudaMalloc(&c16, (size_t)(n_ent + 1) * 16));
+  ow.push_back(e16); ow.push_back(c16);
+  P.ent16 = e16; P.cent16 = c16;
+  if (n_ent) k_pack<<<(n_ent + 127) / 128, 128>>>(P, n_ent, e16, c16);
+  CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   cudaFree(cnt); cudaFree(ccnt); cudaFree(tmp);
   // ---- launch geometry: largest shared-state capacity S that still keeps
@@ -1678,12 +1895,19 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
   {
+    // Shared-memory budget per resident warp: counters for SC tasks, GC parameter
+    // shards and RC staged overlap offsets.  Pick the largest capacities that keep
+    // `target` resident warps per SM (default 8: 1024 chains on 148 SMs).
     size_t tb = al16(tab_bytes_of(P));
-    const int caps[] = {1 << 30, 1024, 768, 640, 512, 384, 256, 192, 128, 64, 0};
-    int bestS = -1, bestW = 0, bestWarps = 0;
+    int target = 8;
+    if (const char *e = getenv("PS_TARGET_WARPS_PER_SM")) target = std::max(1, atoi(e));
+    int bestSC = -1, bestW = 0, bestWarps = 0, bestRC = 0, bestGC = 0;
+    const int caps[] = {4096, 3072, 2048, 1536, 1280, 1024, 896, 768, 640, 512, 384, 256, 128, 0};
     for (int ci = 0; ci < (int)(sizeof caps / sizeof caps[0]); ++ci) {
-      int S = std::min(caps[ci], P.n_slots);
-      size_t wb = al16(warp_bytes_of(P, S));
+      int SC = caps[ci];
+      int GC = std::max(0, SC / 4);
+      int RC = std::max(64, SC / 2);
+      size_t wb = al16(warp_bytes_of(P, SC, GC, RC));
       int cw = 0, cwp = 0;
       for (int wp : {4, 2, 1}) {
         size_t blk = tb + wp * wb;
@@ -1692,13 +1916,17 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
         int warps = std::min(64, blocks * wp);
         if (warps > cw) { cw = warps; cwp = wp; }
       }
-      if (cw > bestWarps) { bestWarps = cw; bestS = S; bestW = cwp; }
-      if (cw >= 8) { bestWarps = cw; bestS = S; bestW = cwp; break; }
+      if (cw > bestWarps || (cw >= target && bestWarps < target)) {
+        bestWarps = cw; bestSC = SC; bestW = cwp; bestRC = RC; bestGC = GC;
+      }
+      if (cw >= target) break;
     }
-    if (bestS < 0) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "problem too large for shared memory"); }
+    if (bestSC < 0) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "problem too large for shared memory"); }
     pr->lay.tab_bytes = tb;
-    pr->lay.warp_bytes = al16(warp_bytes_of(P, bestS));
-    pr->lay.S = bestS;
+    pr->lay.SC = bestSC;
+    pr->lay.GC = bestGC;
+    pr->lay.RC = bestRC;
+    pr->lay.warp_bytes = al16(warp_bytes_of(P, bestSC, bestGC, bestRC));
     pr->wpb = bestW;
     pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
     pr->blocks_per_sm = std::max(1, bestWarps / bestW);
@@ -1734,6 +1962,9 @@ int ps_problem_info_get(const ps_problem *pr, ps_problem_info *o) {
   o->ready_capacity = pr->P.cap;
   o->warps_per_block = pr->wpb;
   o->device_bytes = pr->device_bytes;
+  o->shared_counters = pr->lay.SC;
+  o->resident_warps_per_sm = pr->blocks_per_sm * pr->wpb;
+  o->smem_per_block = (int32_t)pr->smem_per_block;
   return PS_OK;
 }
 
@@ -2004,6 +2235,21 @@ int ps_mcmc_stop(ps_mcmc *m, const uint8_t *stop) {
 
 
 int ps_mcmc_chains(const ps_mcmc *m) { return m ? m->n : 0; }
+
+int ps_debug_phases(unsigned long long *out, int reset) {
+#ifdef PS_PHASES
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    CK(cudaMemcpyToSymbol(g_phase, z, sizeof z));
+  }
+  return PS_OK;
+#else
+  (void)out; (void)reset;
+  return fail(PS_ERR_INVALID, "built without PS_PHASES");
+#endif
+}
 
 int ps_mcmc_read_state(ps_mcmc *m, int32_t *maps, uint8_t *assign) {
   if (!m) return fail(PS_ERR_INVALID, "bad arguments");
