@@ -96,6 +96,7 @@ typedef struct ps_problem_desc {
   const int32_t *combo_off;           /* [n_pairs+1] (src map, dst map) combos per pair */
   const int32_t *combo_row_off;       /* [n_combos+1] prefix of src map sizes */
   const int32_t *combo_col_off;       /* [n_combos+1] prefix of dst map sizes */
+  double backward_multiplier;         /* exe_bwd == exe_fwd * this (cost.py:111) */
 } ps_problem_desc;
 
 typedef struct ps_problem_info {

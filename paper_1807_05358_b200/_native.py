@@ -46,6 +46,7 @@ class PsProblemDesc(ctypes.Structure):
         ("map_shard", c_dbl_p), ("map_ngroups", c_int_p),
         ("pair_src", c_int_p), ("pair_dst", c_int_p), ("pair_need_off", c_int_p), ("need", c_int_p),
         ("combo_off", c_int_p), ("combo_row_off", c_int_p), ("combo_col_off", c_int_p),
+        ("backward_multiplier", ctypes.c_double),
     ]
 
 

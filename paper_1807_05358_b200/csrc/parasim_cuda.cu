@@ -69,6 +69,7 @@ struct DevProb {
   const unsigned short *ent_k, *ent_l;
   const long long *ent_bytes;
   const void *ent16, *cent16;  // packed (k | l << 16, bytes) rows and column-ordered copies
+  double mult;                 // backward_multiplier (exe_bwd == exe_fwd * mult, one IEEE product)
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
@@ -659,9 +660,9 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(4 * (size_t)(P.n_ops + 1)) * 2;          // fbase, gbase
   b += al16(4 * (size_t)P.n_pairs) * 2;              // prow, pcol
   b += al16((size_t)P.n_slots);                      // asg
-  b += al16(8 * (size_t)P.n_queues) * 3;             // qclock, qready, qbest
+  b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
-  b += al16(8 * (size_t)P.n_ops) * 2;                // per-op exe cache (single device kind)
+  b += al16(8 * (size_t)P.n_ops) + 16;               // per-op forward exe cache, flags
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
@@ -676,7 +677,8 @@ struct W2 {
   unsigned long long *qready, *qbest, *rhi, *rlo;
   double *rexe;
   int *rq, *mem;
-  double *exef, *exeb;
+  double *exef;
+  int *flags;  // [0]: slow-path queue bids may be dirty
   double *cready;
   unsigned short *crem;
   unsigned char *cgrp;
@@ -735,15 +737,13 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.pcol = (int *)take(4 * P.n_pairs);
   w.asg = (unsigned char *)take(P.n_slots);
   w.qclock = (double *)take(8 * P.n_queues);
-  w.qready = (unsigned long long *)take(8 * P.n_queues);
-  w.qbest = (unsigned long long *)take(8 * P.n_queues);
   w.rhi = (unsigned long long *)take(8 * P.cap);
   w.rlo = (unsigned long long *)take(8 * P.cap);
   w.rexe = (double *)take(8 * P.cap);
   w.rq = (int *)take(4 * P.cap);
   w.mem = (int *)take(4 * P.cap);
   w.exef = (double *)take(8 * P.n_ops);
-  w.exeb = (double *)take(8 * P.n_ops);
+  w.flags = (int *)take(16);
   w.cready = (double *)take(8 * L.SC);
   w.crem = (unsigned short *)take(2 * L.SC);
   w.cgrp = (unsigned char *)take(L.SC);
@@ -763,9 +763,17 @@ struct State {  // one candidate's dense counters (shared memory, or a global sl
   int Tf, G;
 };
 
-__host__ __device__ inline size_t gscratch_bytes(int n_slots) {
+__host__ __device__ inline size_t gscratch_bytes(int n_slots, int n_queues) {
   return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 2) + al16((size_t)n_slots) +
-         al16((size_t)n_slots * 8) + 128;
+         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + 128;
+}
+
+// slow-path per-queue bid arrays (ready bits, origin key): tail of the warp's global slice
+__device__ inline void bind_bids(const DevProb &P, char *gscratch, W2 &w) {
+  char *g = gscratch + al16((size_t)P.n_slots * 3 * 8) + al16((size_t)P.n_slots * 3 * 2) + al16((size_t)P.n_slots) +
+            al16((size_t)P.n_slots * 8);
+  w.qready = (unsigned long long *)g;
+  w.qbest = w.qready + P.n_queues;
 }
 
 __device__ __forceinline__ bool push2(bool want, double ready, unsigned long long key, double exe, int q, int &n,
@@ -831,7 +839,7 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
       w.gmap[o] = g;
       sz = P.map_size[g];
       ng = T.op_param_mask[o] >= 0 ? P.map_ngroups[g] : 0;
-      if (P.n_kinds == 1) { w.exef[o] = P.exe_fwd[g]; w.exeb[o] = P.exe_bwd[g]; }
+      if (P.n_kinds == 1) w.exef[o] = P.exe_fwd[g];
     }
     int a = sz, b = ng;
 #pragma unroll
@@ -923,7 +931,7 @@ __device__ __forceinline__ void op_attrs(const DevProb &P, const Tab &T, const W
                                          int &q, double &exe) {
   int dev = w.asg[T.op_slot_off[a] + c];
   q = dev;
-  if (P.n_kinds == 1) exe = (kind == KIND_OP ? w.exef : w.exeb)[a];
+  if (P.n_kinds == 1) exe = kind == KIND_OP ? w.exef[a] : __dmul_rn(w.exef[a], P.mult);
   else exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
 }
 
@@ -963,7 +971,13 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   PH_CNT(10, (P.full ? 2 * Tf + st.G : Tf) <= L.SC ? 1 : 0);
   const Ent16 *ent = (const Ent16 *)P.ent16;
   const Ent16 *cent = (const Ent16 *)P.cent16;
-  for (int q = lane; q < P.n_queues; q += 32) { w.qclock[q] = 0.0; w.qready[q] = ~0ull; w.qbest[q] = ~0ull; }
+  const bool was_dirty = w.flags[0] != 0;
+  for (int q = lane; q < P.n_queues; q += 32) {
+    w.qclock[q] = 0.0;
+    if (was_dirty) { w.qready[q] = ~0ull; w.qbest[q] = ~0ull; }
+  }
+  __syncwarp();
+  if (lane == 0) w.flags[0] = 0;
   if (P.full)
     for (int s = lane; s < st.G; s += 32) st.gmask[s] = 0ull;
   __syncwarp();
@@ -1032,6 +1046,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     PH_T(t_sel);
     PH_CNT(11, 1);
     PH_CNT(12, n);
+    unsigned wbits = 0;  // lanes holding this round's winners
+    bool mine = false;
     int nw = 0;
     unsigned long long mykey = 0;
     double myready = 0.0, myexe = 0.0;
@@ -1068,22 +1084,19 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       unsigned wb = __ballot_sync(FULLMASK, win);
       nw = __popc(wb);
-      if (win) { w.qbest[q] = ~0ull; w.qready[q] = ~0ull; }  // clears a bid left by an earlier capped round
+      if (win && w.flags[0]) { w.qbest[q] = ~0ull; w.qready[q] = ~0ull; }  // bid left by a capped slow round
       bool keep = valid && !win;
       unsigned kb = __ballot_sync(FULLMASK, keep);
-      __syncwarp();
       if (keep) {
         int pos = __popc(kb & ((1u << lane) - 1u));
         w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = q;
       }
       n = __popc(kb);
-      int src = lane < nw ? (int)__fns(wb, 0, lane + 1) : 0;
-      mykey = __shfl_sync(FULLMASK, k, src);
-      myready = __shfl_sync(FULLMASK, r, src);
-      myexe = __shfl_sync(FULLMASK, e, src);
-      myq = __shfl_sync(FULLMASK, q, src);
-      __syncwarp();
+      wbits = wb;
+      mine = win;
+      mykey = k; myready = r; myexe = e; myq = q;
     } else {
+      if (lane == 0) w.flags[0] = 1;
       // ---- scan 1: minimum key and LB = min(ready + exe)
       unsigned long long bh = ~0ull, bl = ~0ull, lb = ~0ull;
       for (int i = lane; i < n; i += 32) {
@@ -1167,8 +1180,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         n -= nw;
         __syncwarp();
       }
+      mine = lane < nw;
+      wbits = nw == 32 ? FULLMASK : ((1u << nw) - 1u);
     }
-    bool mine = lane < nw;
     // ---- run the winners: distinct queues, each its queue's next task
     double end = 0.0;
     if (mine) {
@@ -1187,7 +1201,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int G = 32 >> lg, lgG = 5 - lg;
     int wi = lane >> lgG, j0 = lane & (G - 1);
     bool act_lane = wi < nw;
-    int srcl = act_lane ? wi : 0;
+    int srcl = act_lane ? (int)__fns(wbits, 0, wi + 1) : 0;
     unsigned long long wkey = __shfl_sync(FULLMASK, mykey, srcl);
     double wend = __shfl_sync(FULLMASK, end, srcl);
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
@@ -1367,7 +1381,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   return out;
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
                  double *makespan, int *status, char *gscratch) {
   extern __shared__ __align__(16) char smem[];
@@ -1379,7 +1393,10 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
   W2 w;
   carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay, w);
   int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
-  char *gs = gscratch + (size_t)gw * gscratch_bytes(P.n_slots);
+  char *gs = gscratch + (size_t)gw * gscratch_bytes(P.n_slots, P.n_queues);
+  bind_bids(P, gs, w);
+  if (lane == 0) w.flags[0] = 1;  // the global bid arrays start uninitialised
+  __syncwarp();
   for (int cand = gw; cand < n; cand += nw) {
     const int *m = maps + (size_t)cand * P.n_ops;
     const unsigned char *a = asgs + (size_t)cand * P.n_slots;
@@ -1566,7 +1583,7 @@ struct WarpRng {
   }
 };
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns) {
@@ -1580,7 +1597,10 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   if (chain >= n_chains) return;
   W2 w;
   carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay, w);
-  char *gs = gscratch + (size_t)chain * gscratch_bytes(P.n_slots);
+  char *gs = gscratch + (size_t)chain * gscratch_bytes(P.n_slots, P.n_queues);
+  bind_bids(P, gs, w);
+  if (lane == 0) w.flags[0] = 1;
+  __syncwarp();
   int *gmapl = maps + (size_t)chain * P.n_ops;
   unsigned char *gasg = asgs + (size_t)chain * P.n_slots;
   ChainState cs = st[chain];
@@ -1799,7 +1819,8 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   P.n_ops = d->n_ops; P.n_dev = d->n_devices; P.n_kinds = d->n_kinds; P.n_links = d->n_links;
   P.n_pairs = d->n_pairs; P.n_maps = d->n_maps; P.full = d->mode_full; P.n_slots = d->n_slots;
   P.n_queues = d->n_devices + d->n_links;
-  P.cap = d->ready_capacity > 0 ? d->ready_capacity : 256;
+  P.cap = d->ready_capacity > 0 ? d->ready_capacity : 128;
+  P.mult = d->backward_multiplier;
   std::vector<void *> &ow = pr->owned;
   int n_combos = 0;
   n_combos = d->combo_off[d->n_pairs];
@@ -1899,17 +1920,17 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
     // shards and RC staged overlap offsets.  Pick the largest capacities that keep
     // `target` resident warps per SM (default 8: 1024 chains on 148 SMs).
     size_t tb = al16(tab_bytes_of(P));
-    int target = 8;
+    int target = 7;  // 7 x 148 SMs = 1036 resident chains >= the 1024-chain workload
     if (const char *e = getenv("PS_TARGET_WARPS_PER_SM")) target = std::max(1, atoi(e));
     int bestSC = -1, bestW = 0, bestWarps = 0, bestRC = 0, bestGC = 0;
     const int caps[] = {4096, 3072, 2048, 1536, 1280, 1024, 896, 768, 640, 512, 384, 256, 128, 0};
     for (int ci = 0; ci < (int)(sizeof caps / sizeof caps[0]); ++ci) {
       int SC = caps[ci];
-      int GC = std::max(0, SC / 4);
-      int RC = std::max(64, SC / 2);
+      int GC = std::max(16, SC / 4);
+      int RC = std::max(64, 3 * SC / 4);
       size_t wb = al16(warp_bytes_of(P, SC, GC, RC));
       int cw = 0, cwp = 0;
-      for (int wp : {4, 2, 1}) {
+      for (int wp : {8, 7, 6, 5, 4, 3, 2, 1}) {
         size_t blk = tb + wp * wb;
         if (blk > (size_t)optin) continue;
         int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
@@ -2020,7 +2041,7 @@ int ps_simulate_batch(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   if (warps > pr->scratch_warps) {
     cudaFree(pr->scratch);
     size_t want = (size_t)pr->sm_count * pr->blocks_per_sm * wpb;
-    CK(cudaMalloc(&pr->scratch, want * gscratch_bytes(pr->P.n_slots)));
+    CK(cudaMalloc(&pr->scratch, want * gscratch_bytes(pr->P.n_slots, pr->P.n_queues)));
     pr->scratch_warps = want;
   }
   k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch);
@@ -2146,7 +2167,7 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
-  CK(cudaMalloc(&m->scratch, (size_t)n * gscratch_bytes(P.n_slots)));
+  CK(cudaMalloc(&m->scratch, (size_t)n * gscratch_bytes(P.n_slots, P.n_queues)));
   CK(cudaMalloc(&m->d_best, sizeof(double)));
   CK(cudaMalloc(&m->d_bestc, sizeof(int)));
   CK(cudaMemcpy(m->maps, init_map, (size_t)n * P.n_ops * sizeof(int), cudaMemcpyHostToDevice));

@@ -70,7 +70,7 @@ class Lowered:
     slot_off: np.ndarray
     pairs: list[tuple[int, int]]
     arrays: dict = field(default_factory=dict)
-    ready_capacity: int = 256
+    ready_capacity: int = 128
     device: int = 0
     _handle: object = None
     fingerprint: tuple = ()
@@ -110,6 +110,7 @@ class Lowered:
             for name in ("link_bw", "link_lat", "exe_fwd", "exe_bwd", "map_shard"):
                 setattr(d, name, p(name, ctypes.c_double))
             d.op_dim = p("op_dim", ctypes.c_int64)
+            d.backward_multiplier = float(self.profile.backward_multiplier)
             h = ctypes.c_void_p()
             nat.check(L.ps_problem_create(ctypes.byref(d), self.device, ctypes.byref(h)), "ps_problem_create")
             self._handle = h
@@ -183,7 +184,7 @@ class Lowered:
 
 
 def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree: int | None = None,
-          strategies=(), ready_capacity: int = 256, device: int = 0) -> Lowered:
+          strategies=(), ready_capacity: int = 128, device: int = 0) -> Lowered:
     """Flatten a problem.  ``max_degree`` adds every enumerate_configs map (the
     MCMC proposal space); ``strategies`` adds the maps those strategies use."""
     if mode not in (MODE_FORWARD, MODE_FULL):

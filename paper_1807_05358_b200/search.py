@@ -149,8 +149,12 @@ def _eval_encoded(low, maps, asg, strategies=None):
     n = maps.shape[0]
     mk = np.zeros(n, dtype=np.float64)
     st = np.zeros(n, dtype=np.int32)
-    nat.check(nat.lib().ps_simulate_batch(low.handle(), nat.ptr(maps), nat.ptr(asg), n, nat.ptr(mk), nat.ptr(st),
-                                          nat.PS_HOST_PTRS, None), "ps_simulate_batch")
+    while True:
+        nat.check(nat.lib().ps_simulate_batch(low.handle(), nat.ptr(maps), nat.ptr(asg), n, nat.ptr(mk),
+                                              nat.ptr(st), nat.PS_HOST_PTRS, None), "ps_simulate_batch")
+        if not np.any(st == nat.PS_STATUS_CAPACITY):
+            break
+        low = _regrow(low)  # a ready set outgrew its shared-memory capacity: 4x capacity
     bad = np.nonzero(st)[0]
     if bad.size:
         i = int(bad[0])
@@ -159,6 +163,16 @@ def _eval_encoded(low, maps, asg, strategies=None):
         _bind(tg, low)
         _raise_status(tg, int(st[i]))
     return mk
+
+
+def _regrow(low):
+    """The same lowered problem with a 4x larger ready-set capacity (identical
+    map tables, so encoded strategies stay valid)."""
+    import copy
+    new = copy.copy(low)
+    new._handle = None
+    new.ready_capacity = low.ready_capacity * 4
+    return new
 
 
 # -----------------------------------------------------------------------------
@@ -197,7 +211,13 @@ def mcmc_search(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile,
     if live:
         low = lower(g, topo, profile, params.mode, max_degree=params.max_degree,
                     strategies=[initial[c] for c in live], device=params.device)
-        _run_chains(low, params, initial, live, summaries, traces, best, start_err)
+        while True:
+            summaries = [None] * n
+            traces = [[] for _ in range(n)]
+            best = {}
+            if _run_chains(low, params, initial, live, summaries, traces, best, start_err):
+                break
+            low = _regrow(low)  # some chain's ready set outgrew shared memory: rerun, same streams
     for ci, msg in start_err.items():
         if summaries[ci] is None:
             _logger.warning("chain %d failed to start: %s", ci, msg[len("error: "):])
@@ -221,7 +241,8 @@ def mcmc_search(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile,
                         chains=list(summaries))
 
 
-def _run_chains(low, params, initial, live, summaries, traces, best, start_err):
+def _run_chains(low, params, initial, live, summaries, traces, best, start_err) -> bool:
+    """Runs the chains; False if a chain hit the ready-set capacity (caller regrows)."""
     from .taskgraph import NoRouteError, TaskGraph, _bind, _first_missing_route
     L = nat.lib()
     n = len(live)
@@ -299,7 +320,8 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err):
         tok = np.zeros((n, max(record, 1)), dtype=np.uint8)
         nat.check(L.ps_mcmc_read(h, summ, nat.ptr(bmaps), nat.ptr(basg), nat.ptr(tc) if record else None,
                                  nat.ptr(tok) if record else None), "ps_mcmc_read")
-        cur_maps = None
+        if any(summ[i].status == nat.PS_STATUS_CAPACITY for i in range(n)):
+            return False
         for i, ci in enumerate(live):
             s = summ[i]
             termination = term[i]
@@ -314,8 +336,6 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err):
                 a, b = _proposal_route_error(low, h, i, int(s.last_op))
                 termination = f"error: no route between device {a} and device {b}"
                 _logger.warning("chain %d aborted after %d proposals: %s", ci, s.proposals, termination[7:])
-            elif s.status == nat.PS_STATUS_CAPACITY:
-                termination = "error: ready-set capacity exceeded"
             summaries[ci] = ChainSummary(ci, s.initial_cost, s.best_cost, int(s.proposals), int(s.accepted),
                                          s.beta, termination)
             if record:
@@ -324,6 +344,7 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err):
             best[ci] = (s.best_cost, low.decode(bmaps[i], basg[i], template=initial[ci]))
     finally:
         L.ps_mcmc_destroy(h)
+    return True
 
 
 def _proposal_route_error(low, h, i, op_rank):

@@ -328,11 +328,12 @@ def build_task_graph(g: OperatorGraph, topo: DeviceTopology, strategy: Paralleli
 
 
 def _grow(tg: TaskGraph):
-    low = tg._low
-    new = lower(low.graph, low.topology, low.profile, low.mode, max_degree=low.max_degree,
-                strategies=[tg.strategy], ready_capacity=low.ready_capacity * 4, device=low.device)
+    from .search import _regrow
+    new = _regrow(tg._low)
     try:
-        tg.profile.__dict__[_LOWER_CACHE_ATTR] = None
+        cache = tg.profile.__dict__.get(_LOWER_CACHE_ATTR)
+        if cache is not None and cache[1] is tg._low:
+            tg.profile.__dict__[_LOWER_CACHE_ATTR] = (cache[0], new, cache[2])
     except (AttributeError, TypeError):
         pass
     _bind(tg, new)

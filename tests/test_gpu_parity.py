@@ -151,3 +151,33 @@ def test_missing_link_is_reported_like_the_reference():
         "b": ps.ParallelizationConfig({"sample": 1, "channel": 1}, ("d2",))})
     with pytest.raises(ps.NoRouteError, match="no route between device d0 and device d2"):
         ps.build_task_graph(g, topo, strat, ps.CostProfile(), ps.MODE_FORWARD)
+
+
+def test_ready_set_capacity_regrows_transparently(oracle):
+    """A deliberately tiny ready-set capacity must still give the exact answer
+    (the problem is regrown 4x until every candidate fits)."""
+    from paper_1807_05358_b200.lowering import lower
+    from paper_1807_05358_b200.search import _eval_encoded
+    g = ps.nmt_like(steps=4, layers=2, batch=64, hidden=64, vocab=64)
+    topo = ps.multi_node_topology(4, 4)
+    prof = ps.CostProfile()
+    strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, 4, s) for s in range(3)]
+    for mode in (ps.MODE_FORWARD, ps.MODE_FULL):
+        low = lower(g, topo, prof, mode, max_degree=4, strategies=strategies, ready_capacity=2)
+        maps = np.zeros((len(strategies), low.n_ops), dtype=np.int32)
+        asg = np.zeros((len(strategies), low.n_slots), dtype=np.uint8)
+        for i, s in enumerate(strategies):
+            low.encode(s, maps[i], asg[i])
+        got = _eval_encoded(low, maps, asg, strategies)
+        assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies))
+
+
+def test_large_ready_sets_take_the_multi_chunk_path(oracle):
+    """NMT data-parallel graphs put > 32 tasks in the ready set at once."""
+    g = ps.nmt_like(steps=8, layers=2, batch=64, hidden=64, vocab=64)
+    topo = ps.multi_node_topology(4, 4)
+    prof = ps.CostProfile()
+    strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, 8, s) for s in range(3)]
+    for mode in (ps.MODE_FORWARD, ps.MODE_FULL):
+        got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=8)
+        assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies))
