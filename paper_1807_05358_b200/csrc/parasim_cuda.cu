@@ -662,7 +662,7 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16((size_t)P.n_slots);                      // asg
   b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
-  b += al16(8 * (size_t)P.n_ops) + 16;               // per-op forward exe cache, flags
+  b += al16(8 * (size_t)P.n_ops) + 16 + 128;         // per-op forward exe cache, flags, winner lanes
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
@@ -679,6 +679,7 @@ struct W2 {
   int *rq, *mem;
   double *exef;
   int *flags;  // [0]: slow-path queue bids may be dirty
+  int *wlane;  // [32] lane holding the k-th winner of the round
   double *cready;
   unsigned short *crem;
   unsigned char *cgrp;
@@ -744,6 +745,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.mem = (int *)take(4 * P.cap);
   w.exef = (double *)take(8 * P.n_ops);
   w.flags = (int *)take(16);
+  w.wlane = (int *)take(128);
   w.cready = (double *)take(8 * L.SC);
   w.crem = (unsigned short *)take(2 * L.SC);
   w.cgrp = (unsigned char *)take(L.SC);
@@ -1094,6 +1096,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       n = __popc(kb);
       wbits = wb;
       mine = win;
+      if (win) w.wlane[__popc(wb & ((1u << lane) - 1u))] = lane;
       mykey = k; myready = r; myexe = e; myq = q;
     } else {
       if (lane == 0) w.flags[0] = 1;
@@ -1182,6 +1185,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       mine = lane < nw;
       wbits = nw == 32 ? FULLMASK : ((1u << nw) - 1u);
+      w.wlane[lane] = lane;
     }
     // ---- run the winners: distinct queues, each its queue's next task
     double end = 0.0;
@@ -1201,7 +1205,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int G = 32 >> lg, lgG = 5 - lg;
     int wi = lane >> lgG, j0 = lane & (G - 1);
     bool act_lane = wi < nw;
-    int srcl = act_lane ? (int)__fns(wbits, 0, wi + 1) : 0;
+    __syncwarp();
+    int srcl = act_lane ? w.wlane[wi] : 0;
     unsigned long long wkey = __shfl_sync(FULLMASK, mykey, srcl);
     double wend = __shfl_sync(FULLMASK, end, srcl);
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
@@ -1381,7 +1386,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   return out;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
                  double *makespan, int *status, char *gscratch) {
   extern __shared__ __align__(16) char smem[];
@@ -1583,7 +1588,7 @@ struct WarpRng {
   }
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns) {
