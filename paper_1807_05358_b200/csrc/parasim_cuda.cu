@@ -1333,31 +1333,24 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           if (!sync_attrs(P, T, w, st, a, b, c + 1, pq, pexe, ea, eb)) err = true;
         }
       }
-      // arrivals at the same counter in this iteration merge into one update by
-      // the group's lowest lane (max of the ends, count of arrivals): no atomics
-      unsigned gm = __match_any_sync(FULLMASK, act == 1 ? slot : (0x40000000 | lane));
+      // arrivals: every max lands before any count reaches zero (the warp
+      // barrier orders them); the u16 counter is decremented through the
+      // 32-bit word that holds it (no borrow: it stops at zero)
+      if (act == 1) atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(wend));
+      __syncwarp();
       bool want = false;
       double pready = 0.0;
       if (act == 1) {
-        double gmax = wend;
-        if (__popc(gm) > 1) {
-          unsigned long long eb64 = (unsigned long long)__double_as_longlong(wend);
-          unsigned hi = __reduce_max_sync(gm, (unsigned)(eb64 >> 32));
-          unsigned lo = __reduce_max_sync(gm, (unsigned)(eb64 >> 32) == hi ? (unsigned)eb64 : 0u);
-          gmax = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
-        }
-        if (lane == __ffs(gm) - 1) {
-          double rr = st.ready[slot];
-          if (gmax > rr) { rr = gmax; st.ready[slot] = rr; }
-          int left = (int)st.rem[slot] - __popc(gm);
-          st.rem[slot] = (unsigned short)left;
-          if (left == 0) {
-            want = true;
-            pready = rr;
-            unsigned sk = key_kind(skey);
-            op_attrs(P, T, w, sk == KIND_SYNC ? KIND_OP : sk, key_a(skey), key_c(skey), pq, pexe);
-            if (sk == KIND_SYNC && !sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb))
-              err = true;
+        unsigned sh = (slot & 1) * 16;
+        unsigned old = atomicSub((unsigned *)(st.rem + (slot & ~1)), 1u << sh);
+        if (((old >> sh) & 0xffffu) == 1u) {
+          want = true;
+          pready = st.ready[slot];
+          unsigned sk = key_kind(skey);
+          if (sk == KIND_SYNC) {
+            if (!sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb)) err = true;
+          } else {
+            op_attrs(P, T, w, sk, key_a(skey), key_c(skey), pq, pexe);
           }
         }
       } else if (act == 2) {
