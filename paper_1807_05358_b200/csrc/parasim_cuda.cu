@@ -663,6 +663,7 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
   b += al16(8 * (size_t)P.n_ops) + 16 + 128;         // per-op forward exe cache, flags, winner lanes
+  b += al16(4 * (size_t)P.n_queues);                 // queue claims
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
@@ -680,6 +681,7 @@ struct W2 {
   double *exef;
   int *flags;  // [0]: slow-path queue bids may be dirty
   int *wlane;  // [32] lane holding the k-th winner of the round
+  int *qown;   // [Q] last member to claim the queue this round
   double *cready;
   unsigned short *crem;
   unsigned char *cgrp;
@@ -746,6 +748,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.exef = (double *)take(8 * P.n_ops);
   w.flags = (int *)take(16);
   w.wlane = (int *)take(128);
+  w.qown = (int *)take(4 * P.n_queues);
   w.cready = (double *)take(8 * L.SC);
   w.crem = (unsigned short *)take(2 * L.SC);
   w.cgrp = (unsigned char *)take(L.SC);
@@ -1069,10 +1072,15 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int wl = warp_argmin128(h, k, lane);
         member = lane == wl;
       }
-      // per-queue minimum (ready, origin) among members: a member alone on its
-      // queue wins outright; ties on a queue take a group-restricted lexicographic min
-      unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
+      // per-queue minimum (ready, origin) among members: each member claims its
+      // queue; a member alone on its queue wins outright, and only queues claimed
+      // twice take a group-restricted lexicographic min
+      if (member) w.qown[q] = lane;
+      __syncwarp();
+      bool lost = member && w.qown[q] != lane;
       bool win = member;
+      if (__any_sync(FULLMASK, lost)) {
+      unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
       if (member && __popc(gm) > 1) {
         unsigned cand = gm, v, mn;
         v = (unsigned)(h >> 32); mn = __reduce_min_sync(gm, v); cand &= __ballot_sync(gm, v == mn);
@@ -1083,6 +1091,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         v = (cand >> lane & 1) ? (unsigned)k : 0xffffffffu; mn = __reduce_min_sync(gm, v);
         cand &= __ballot_sync(gm, v == mn);
         win = (__ffs(cand) - 1) == lane;
+      }
       }
       unsigned wb = __ballot_sync(FULLMASK, win);
       nw = __popc(wb);
