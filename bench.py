@@ -202,13 +202,15 @@ def run_ours(args):
     C = args.chains
     first = rank * C
     init = initial_strategies(g, topo, md, first, C)
+    from paper_1807_05358_b200.search import fit_capacity
     low = lower(g, topo, prof, args.mode, max_degree=md, strategies=init, device=local)
-    info = low.info()
     L = nat.lib()
     maps = np.zeros((C, low.n_ops), dtype=np.int32)
     asg = np.zeros((C, low.n_slots), dtype=np.uint8)
     for i, s in enumerate(init):
         low.encode(s, maps[i], asg[i])
+    low = fit_capacity(low, maps, asg)  # ready-set capacity from a pilot evaluation of the starts
+    info = low.info()
     seeds = np.array([1000003 * (first + i) for i in range(C)], dtype=np.uint64)
     mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0)
     h = ctypes.c_void_p()

@@ -26,6 +26,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <algorithm>
 #include <string>
@@ -682,6 +683,7 @@ struct W2 {
   int *flags;  // [0]: slow-path queue bids may be dirty
   int *wlane;  // [32] lane holding the k-th winner of the round
   int *qown;   // [Q] last member to claim the queue this round
+  int rcap;    // ready-set capacity in effect (shared memory, or the global overflow slice)
   double *cready;
   unsigned short *crem;
   unsigned char *cgrp;
@@ -757,6 +759,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.scol = (int *)take(4 * L.RC);
   w.oldasg = (unsigned char *)take(256);
   w.ph = (unsigned long long *)take(128);
+  w.rcap = P.cap;
 }
 
 struct State {  // one candidate's dense counters (shared memory, or a global slice)
@@ -768,9 +771,11 @@ struct State {  // one candidate's dense counters (shared memory, or a global sl
   int Tf, G;
 };
 
+__host__ __device__ inline int overflow_cap(int n_slots) { return 4 * n_slots + 1024; }
+
 __host__ __device__ inline size_t gscratch_bytes(int n_slots, int n_queues) {
   return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 2) + al16((size_t)n_slots) +
-         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + 128;
+         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + (size_t)overflow_cap(n_slots) * 32 + 256;
 }
 
 // slow-path per-queue bid arrays (ready bits, origin key): tail of the warp's global slice
@@ -781,12 +786,37 @@ __device__ inline void bind_bids(const DevProb &P, char *gscratch, W2 &w) {
   w.qbest = w.qready + P.n_queues;
 }
 
+// Ready set in the warp's global slice (exact overflow path for wide candidates).
+__device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 w) {
+  char *g = gscratch + al16((size_t)P.n_slots * 3 * 8) + al16((size_t)P.n_slots * 3 * 2) + al16((size_t)P.n_slots) +
+            al16((size_t)P.n_slots * 8) + al16((size_t)P.n_queues * 16);
+  int c = overflow_cap(P.n_slots);
+  w.rhi = (unsigned long long *)g;
+  w.rlo = w.rhi + c;
+  w.rexe = (double *)(w.rlo + c);
+  w.rq = (int *)(w.rexe + c);
+  w.mem = w.rq + c;
+  w.rcap = c;
+  return w;
+}
+
+__device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
+
+// Simulate; a candidate whose ready set outgrows shared memory is re-run with
+// the ready set in global memory (same answer, slower).
+__device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch,
+                                      int lane) {
+  SimOut o = warp_simulate2(P, T, w, L, gscratch, lane);
+  if (o.status == PS_STATUS_CAPACITY) o = warp_simulate2(P, T, with_global_ready_set(P, gscratch, w), L, gscratch, lane);
+  return o;
+}
+
 __device__ __forceinline__ bool push2(bool want, double ready, unsigned long long key, double exe, int q, int &n,
                                       const DevProb &P, const W2 &w, int lane) {
   unsigned bm = __ballot_sync(FULLMASK, want);
   if (!bm) return true;
   int total = __popc(bm);
-  if (n + total > P.cap) return false;
+  if (n + total > w.rcap) return false;
   if (want) {
     int pos = n + __popc(bm & ((1u << lane) - 1u));
     w.rhi[pos] = (unsigned long long)__double_as_longlong(ready);
@@ -1410,7 +1440,7 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
     for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = m[i];
     for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = a[i];
     __syncwarp();
-    SimOut o = warp_simulate2(P, T, w, lay, gs, lane);
+    SimOut o = simulate_any(P, T, w, lay, gs, lane);
     if (lane == 0) {
       makespan[cand] = o.status == PS_STATUS_OK ? o.makespan : -1.0;
       status[cand] = o.status;
@@ -1627,7 +1657,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   int *bmap = best_maps + (size_t)chain * P.n_ops;
   unsigned char *basg = best_asgs + (size_t)chain * P.n_slots;
   if (!cs.started) {
-    SimOut o = warp_simulate2(P, T, w, lay, gs, lane);
+    SimOut o = simulate_any(P, T, w, lay, gs, lane);
     cs.started = 1;
     if (o.status != PS_STATUS_OK) {
       cs.status = o.status; cs.err_a = o.err_a; cs.err_b = o.err_b;
@@ -1677,7 +1707,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     if (same) {
       cand = cs.cost;
     } else {
-      SimOut so = warp_simulate2(P, T, w, lay, gs, lane);
+      SimOut so = simulate_any(P, T, w, lay, gs, lane);
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
         break;
@@ -1959,12 +1989,19 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
     pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
     pr->blocks_per_sm = std::max(1, bestWarps / bestW);
   }
-  CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
-  CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr->smem_per_block));
+  // the attribute is per kernel, not per problem: allow the device maximum so
+  // problems with different layouts can coexist
+  CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
-  if (wsm > 48 * 1024) CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+  if (wsm > (size_t)optin) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "ready set too large for tracing"); }
+  CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch, pr->wpb * 32, pr->smem_per_block));
+  if (getenv("PS_DEBUG"))
+    fprintf(stderr, "[parasim] tab=%zu warp=%zu SC=%d GC=%d RC=%d wpb=%d smem/block=%zu occ=%d optin=%d per_sm=%d\n",
+            pr->lay.tab_bytes, pr->lay.warp_bytes, pr->lay.SC, pr->lay.GC, pr->lay.RC, pr->wpb, pr->smem_per_block, occ,
+            optin, per_sm);
   if (occ < 1) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "kernel does not fit on an SM"); }
   pr->blocks_per_sm = occ;
   pr->device_bytes = 0;

@@ -165,6 +165,28 @@ def _eval_encoded(low, maps, asg, strategies=None):
     return mk
 
 
+def fit_capacity(low, maps, asg, headroom: int = 1):
+    """A problem whose ready-set capacity fits the given candidates with
+    ``headroom``x margin (chains wander; the data-parallel start is usually the
+    widest): evaluates them, regrowing 4x on overflow."""
+    cur = low
+    n = maps.shape[0]
+    mk = np.zeros(n, dtype=np.float64)
+    st = np.zeros(n, dtype=np.int32)
+    while True:
+        nat.check(nat.lib().ps_simulate_batch(cur.handle(), nat.ptr(maps), nat.ptr(asg), n, nat.ptr(mk),
+                                              nat.ptr(st), nat.PS_HOST_PTRS, None), "ps_simulate_batch")
+        if not np.any(st == nat.PS_STATUS_CAPACITY):
+            break
+        cur = _regrow(cur)
+    if headroom > 1:
+        import copy
+        cur = copy.copy(cur)
+        cur._handle = None
+        cur.ready_capacity = cur.ready_capacity * headroom
+    return cur
+
+
 def _regrow(low):
     """The same lowered problem with a 4x larger ready-set capacity (identical
     map tables, so encoded strategies stay valid)."""

@@ -181,3 +181,25 @@ def test_large_ready_sets_take_the_multi_chunk_path(oracle):
     for mode in (ps.MODE_FORWARD, ps.MODE_FULL):
         got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=8)
         assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies))
+
+
+def test_mcmc_chains_survive_ready_set_overflow(oracle):
+    """Chains whose ready set outgrows shared memory re-run that simulation with
+    the ready set in global memory: same trajectory, no failed chains."""
+    from paper_1807_05358_b200.lowering import lower
+    g = ps.nmt_like(steps=4, layers=2, batch=64, hidden=64, vocab=64)
+    topo = ps.multi_node_topology(4, 4)
+    prof = ps.CostProfile()
+    init = [ps.data_parallel_strategy(g, topo), ps.random_strategy(g, topo, 4, 1)]
+    import paper_1807_05358_b200.search as S
+    orig = S.lower
+    S.lower = lambda *a, **k: orig(*a, **{**k, "ready_capacity": 4})
+    try:
+        rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=60, seed=2, max_degree=4, initial=init,
+                                                            polish=False, mode=ps.MODE_FULL, rng="philox"))
+    finally:
+        S.lower = orig
+    ref = oracle.mcmc(g, topo, prof, ps.MODE_FULL, init, [2 + 1000003 * c for c in range(2)], 60, 4,
+                      rng_mode="philox")
+    for ci, ch in enumerate(rep.chains):
+        assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted) == tuple(ref["summary"][ci][:4])
