@@ -126,11 +126,11 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def profiled_traffic():
-    """dram bytes per k_mcmc launch from the committed ncu summary, if any."""
+def profiled_traffic_per_eval():
+    """DRAM bytes per evaluation of k_mcmc from the committed ncu capture, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get("k_mcmc_dram_bytes_per_launch")
+            return json.load(fh).get("k_mcmc_dram_bytes_per_eval")
     except Exception:
         return None
 
@@ -325,6 +325,8 @@ def run_ours(args):
 
     peak, peak_src = measured_peak()
     achieved = bytes_per_eval * (evals / (total_ms / 1e3)) / 1e9  # this rank's kernel, GB/s
+    tpe = profiled_traffic_per_eval()
+    traffic = tpe * evals / args.steps if tpe is not None else None  # DRAM bytes per k_mcmc launch
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -339,8 +341,10 @@ def run_ours(args):
                    "shared_counters": info.shared_counters, "resident_warps_per_sm": info.resident_warps_per_sm,
                    "warps_per_block": info.warps_per_block},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": profiled_traffic(),
-                     "note": f"B_eval = 32*T + 4*E = {bytes_per_eval:.0f} B (SURVEY 8d); peak {peak_src}"},
+                     "frac": achieved / peak, "traffic": traffic,
+                     "note": (f"B_eval = 32*T + 4*E = {bytes_per_eval:.0f} B per evaluation (SURVEY 8d), "
+                              f"{evals / args.steps:.0f} evaluations per launch; peak {peak_src}; "
+                              "traffic from profiles/traffic.json (ncu)")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
