@@ -130,6 +130,12 @@ int ps_combo_entries(ps_problem *prob, int pair, int src_map, int dst_map, int c
 int ps_simulate_batch(ps_problem *prob, const int32_t *map_local, const uint8_t *assign, int n,
                       double *makespan_out, int32_t *status_out, int flags, void *stream);
 
+/* As ps_simulate_batch, plus op_min_end_out [n][n_ops]: the earliest end of each
+ * op's forward tasks (the bound exhaustive_optimal prunes with, search.py:380-381). */
+int ps_simulate_batch_ex(ps_problem *prob, const int32_t *map_local, const uint8_t *assign, int n,
+                         double *makespan_out, int32_t *status_out, double *op_min_end_out, int flags,
+                         void *stream);
+
 /* One strategy with the full timeline.  Tasks are reported in pop order. */
 typedef struct ps_trace_task {
   uint64_t key;   /* packed origin: kind<<61 | a<<45 | b<<29 | c<<14 | d */

@@ -111,6 +111,7 @@ def lib():
     L.ps_combo_entries.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp,
                                    ctypes.POINTER(ctypes.c_int)]
     L.ps_simulate_batch.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp]
+    L.ps_simulate_batch_ex.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp, vp, ctypes.c_int, vp]
     L.ps_simulate_trace.argtypes = [vp, vp, vp, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
                                     vp, vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_int32), vp]

@@ -684,6 +684,7 @@ struct W2 {
   int *wlane;  // [32] lane holding the k-th winner of the round
   int *qown;   // [Q] last member to claim the queue this round
   int rcap;    // ready-set capacity in effect (shared memory, or the global overflow slice)
+  double *opmin;  // optional [n_ops]: earliest end of each op's forward tasks (exhaustive bounds)
   double *cready;
   unsigned short *crem;
   unsigned char *cgrp;
@@ -760,6 +761,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.oldasg = (unsigned char *)take(256);
   w.ph = (unsigned long long *)take(128);
   w.rcap = P.cap;
+  w.opmin = nullptr;
 }
 
 struct State {  // one candidate's dense counters (shared memory, or a global slice)
@@ -1234,6 +1236,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       end = start + myexe;
       w.qclock[myq] = end;
       if (end > out.makespan) out.makespan = end;
+      if (w.opmin && key_kind(mykey) == KIND_OP)
+        atomicMin((unsigned long long *)&w.opmin[key_a(mykey)], (unsigned long long)__double_as_longlong(end));
     }
     PH_ADD(2, t_sel);
     PH_CNT(13, nw);
@@ -1420,7 +1424,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 
 __global__ void __launch_bounds__(256, 1)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
-                 double *makespan, int *status, char *gscratch) {
+                 double *makespan, int *status, char *gscratch, double *opmin) {
   extern __shared__ __align__(16) char smem[];
   Tab T;
   carve_tab(smem, P, T);
@@ -1439,6 +1443,10 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
     const unsigned char *a = asgs + (size_t)cand * P.n_slots;
     for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = m[i];
     for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = a[i];
+    if (opmin) {
+      w.opmin = opmin + (size_t)cand * P.n_ops;
+      for (int i = lane; i < P.n_ops; i += 32) w.opmin[i] = __longlong_as_double(0x7ff0000000000000ll);
+    }
     __syncwarp();
     SimOut o = simulate_any(P, T, w, lay, gs, lane);
     if (lane == 0) {
@@ -2062,8 +2070,8 @@ int ps_combo_entries(ps_problem *pr, int pair, int src_map, int dst_map, int cap
   return PS_OK;
 }
 
-int ps_simulate_batch(ps_problem *pr, const int32_t *map_local, const uint8_t *assign, int n, double *makespan_out,
-                      int32_t *status_out, int flags, void *stream) {
+int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t *assign, int n, double *makespan_out,
+                         int32_t *status_out, double *op_min_end_out, int flags, void *stream) {
   if (!pr || n < 0) return fail(PS_ERR_INVALID, "bad arguments");
   if (n == 0) return PS_OK;
   CK(cudaSetDevice(pr->device));
@@ -2088,14 +2096,26 @@ int ps_simulate_batch(ps_problem *pr, const int32_t *map_local, const uint8_t *a
     CK(cudaMalloc(&pr->scratch, want * gscratch_bytes(pr->P.n_slots, pr->P.n_queues)));
     pr->scratch_warps = want;
   }
-  k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch);
+  double *dop = nullptr;
+  if (op_min_end_out) {
+    if (flags == PS_DEVICE_PTRS) dop = op_min_end_out;
+    else CK(cudaMalloc(&dop, (size_t)n * pr->P.n_ops * sizeof(double)));
+  }
+  k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop);
   CK(cudaGetLastError());
   if (flags != PS_DEVICE_PTRS) {
     CK(cudaMemcpyAsync(makespan_out, dk, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(status_out, ds, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (dop) CK(cudaMemcpyAsync(op_min_end_out, dop, (size_t)n * pr->P.n_ops * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (dop) cudaFree(dop);
   }
   return PS_OK;
+}
+
+int ps_simulate_batch(ps_problem *pr, const int32_t *map_local, const uint8_t *assign, int n, double *makespan_out,
+                      int32_t *status_out, int flags, void *stream) {
+  return ps_simulate_batch_ex(pr, map_local, assign, n, makespan_out, status_out, nullptr, flags, stream);
 }
 
 int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *assign, int task_cap,

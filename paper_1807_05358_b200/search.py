@@ -295,10 +295,15 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
     try:
         if deterministic:
             done = 0
+            seg = max(1, params.segment)
+            if params.check_interval:
+                seg = int(params.check_interval)
             while True:
-                step = min(cap - done, max(1, params.segment)) if cap else 0
+                step = min(cap - done, seg) if cap else 0
                 nat.check(L.ps_mcmc_run(h, step, None), "ps_mcmc_run")
                 done += step
+                if params.check_interval and step == seg:
+                    _verify_chains(low, h, n, live, summ)
                 if done >= cap:
                     break
             term = ["proposal-limit"] * n
@@ -367,6 +372,24 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
     finally:
         L.ps_mcmc_destroy(h)
     return True
+
+
+def _verify_chains(low, h, n, live, summ):
+    """check_interval (search.py:242-249): every live chain's cached cost must
+    equal a fresh evaluation of its current strategy."""
+    L = nat.lib()
+    nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+    maps = np.zeros((n, low.n_ops), dtype=np.int32)
+    asg = np.zeros((n, low.n_slots), dtype=np.uint8)
+    nat.check(L.ps_mcmc_read_state(h, nat.ptr(maps), nat.ptr(asg)), "ps_mcmc_read_state")
+    ok = [i for i in range(n) if summ[i].status == nat.PS_STATUS_OK]
+    if not ok:
+        return
+    fresh = _eval_encoded(low, maps[ok], asg[ok])
+    for j, i in enumerate(ok):
+        if float(fresh[j]) != summ[i].cost:
+            raise SearchError(f"chain {live[i]}: cached cost {summ[i].cost!r} diverged from fresh "
+                              f"simulation {float(fresh[j])!r}")
 
 
 def _proposal_route_error(low, h, i, op_rank):
@@ -507,7 +530,144 @@ def local_optimality_check(strategy: ParallelizationStrategy, g: OperatorGraph, 
     return None
 
 
+def _canonical_assignments(n: int, used: frozenset, devices_by_kind: dict):
+    """Device tuples of length n up to renaming of still-unused same-kind devices:
+    each slot takes an already-used device or the lowest-id unused device of
+    some kind (reference search.py:285-306)."""
+    def rec(i, used_now, prefix):
+        if i == n:
+            yield tuple(prefix)
+            return
+        options = sorted(used_now)
+        for kind in sorted(devices_by_kind):
+            fresh = next((d for d in devices_by_kind[kind] if d not in used_now), None)
+            if fresh is not None:
+                options.append(fresh)
+        for d in options:
+            prefix.append(d)
+            yield from rec(i + 1, used_now | {d}, prefix)
+            prefix.pop()
+
+    yield from rec(0, used, [])
+
+
+def _prefix_graph(g: OperatorGraph, ops: list) -> OperatorGraph:
+    keep = set(ops)
+    sub = OperatorGraph()
+    for oid in ops:
+        sub.ops[oid] = g.ops[oid]
+    sub.tensors = [e for e in g.tensors if e.src in keep and e.dst in keep]
+    return sub
+
+
 def exhaustive_optimal(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile, max_degree: int = 4,
                        cap: float = 1e9, mode: str = MODE_FORWARD) -> ExhaustiveResult:
-    """Not yet on the GPU path."""
-    raise NotImplementedError("exhaustive_optimal is a next-row item on the B200 path (see DESIGN.md)")
+    """Provably optimal strategy by depth-first branch and bound over canonical
+    configs (reference search.py:321-405): ops in topological order; a node dies
+    when its prefix makespan or the critical-path bound through the remaining
+    ops reaches the incumbent.  The same nodes are visited in the same order;
+    all children of a node are scored in one GPU batch (prefix makespan plus
+    each op's earliest task end), then walked in order with the live incumbent."""
+    from .taskgraph import TaskGraph, _bind, _raise_status
+    order = g.topological_order()
+    maps = {oid: enumerate_configs(g.ops[oid], topo, max_degree) for oid in order}
+    ndev = len(topo.devices)
+    estimate = 1.0
+    for oid in order:
+        estimate *= sum(ndev ** m.size() for m in maps[oid])
+    if estimate > cap:
+        raise SearchSpaceTooLarge(f"estimated search space of {estimate:.3g} strategies exceeds cap {cap:.3g}")
+    devices_by_kind: dict = {}
+    for dev_id in sorted(topo.devices):
+        devices_by_kind.setdefault(topo.devices[dev_id].kind, []).append(dev_id)
+    kind_devices = [topo.devices[ids[0]] for ids in devices_by_kind.values()]
+    min_time = {}
+    for oid in order:
+        op = g.ops[oid]
+        best_t = math.inf
+        for m in maps[oid]:
+            reg = output_region(op, ParallelizationConfig(m.degrees, None), 0)
+            for dev in kind_devices:
+                t = profile.task_exe_time(op, reg, dev)
+                if t < best_t:
+                    best_t = t
+        min_time[oid] = best_t
+    preds = {oid: g.predecessors(oid) for oid in order}
+    lows: dict = {}
+
+    def prefix_low(depth):
+        low = lows.get(depth)
+        if low is None:
+            low = lows[depth] = lower(_prefix_graph(g, order[:depth]), topo, profile, mode, max_degree=max_degree)
+        return low
+
+    seed = data_parallel_strategy(g, topo)
+    best_cost = float(evaluate_strategies(g, topo, profile, [seed], mode=mode)[0])
+    best_strategy = seed
+    configs: dict = {}
+    visited = 0
+    N = len(order)
+
+    def score_children(depth, children):
+        """(makespan, status, op min ends) of configs + each child, on the prefix of depth+1 ops."""
+        low = prefix_low(depth + 1)
+        k = len(children)
+        mm = np.zeros((k, low.n_ops), dtype=np.int32)
+        aa = np.zeros((k, low.n_slots), dtype=np.uint8)
+        op_id = order[depth]
+        for j, cfg in enumerate(children):
+            configs[op_id] = cfg
+            low.encode(ParallelizationStrategy(configs), mm[j], aa[j])
+        mk = np.zeros(k, dtype=np.float64)
+        st = np.zeros(k, dtype=np.int32)
+        opmin = np.zeros((k, low.n_ops), dtype=np.float64)
+        while True:
+            nat.check(nat.lib().ps_simulate_batch_ex(low.handle(), nat.ptr(mm), nat.ptr(aa), k, nat.ptr(mk),
+                                                     nat.ptr(st), nat.ptr(opmin), nat.PS_HOST_PTRS, None),
+                      "ps_simulate_batch_ex")
+            if not np.any(st == nat.PS_STATUS_CAPACITY):
+                break
+            low = lows[depth + 1] = _regrow(low)
+        return low, mk, st, opmin
+
+    def visit(depth, used, makespan, min_end_row, low):
+        nonlocal best_cost, best_strategy, visited
+        visited += 1
+        if depth > 0:
+            if makespan >= best_cost:
+                return
+            if depth == N:
+                best_cost = makespan
+                best_strategy = ParallelizationStrategy(dict(configs))
+                return
+            min_end = {oid: float(min_end_row[low.rank[oid]]) for oid in order[:depth]}
+            bound = makespan
+            ec: dict = {}
+            for oid in order[depth:]:
+                base = 0.0
+                for p in preds[oid]:
+                    c = min_end[p] if p in min_end else ec.get(p, 0.0)
+                    if c > base:
+                        base = c
+                ec[oid] = base + min_time[oid]
+                if ec[oid] > bound:
+                    bound = ec[oid]
+            if bound >= best_cost:
+                return
+        elif not order:
+            return
+        op_id = order[depth]
+        children = [(ParallelizationConfig(dict(m.degrees), a), a) for m in maps[op_id]
+                    for a in _canonical_assignments(m.size(), used, devices_by_kind)]
+        clow, mk, st, opmin = score_children(depth, [c for c, _ in children])
+        for j, (cfg, a) in enumerate(children):
+            configs[op_id] = cfg
+            if st[j] != nat.PS_STATUS_OK:  # raise where the reference's build would
+                tg = TaskGraph(clow.graph, topo, ParallelizationStrategy(dict(configs)), profile, mode)
+                _bind(tg, clow)
+                _raise_status(tg, int(st[j]))
+            visit(depth + 1, used | set(a), float(mk[j]), opmin[j], clow)
+        configs.pop(op_id, None)
+
+    visit(0, frozenset(), 0.0, None, None)
+    return ExhaustiveResult(best_strategy, best_cost, visited, estimate)

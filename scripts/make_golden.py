@@ -125,6 +125,51 @@ def mcmc_cases():
     return out
 
 
+def search_report_cases():
+    """Default mcmc_search (MT19937, polish on) -> the reference's own report JSON."""
+    out = []
+    tiny = R.OperatorGraph()
+    tiny.add_op(R.Operation("a", R.OperatorKind("MatMul"), (R.shape(("sample", 4), ("channel", 4)),),
+                            R.shape(("sample", 4), ("channel", 4)), param_bytes=64))
+    tiny.add_op(R.Operation("b", R.OperatorKind("MatMul"), (R.shape(("sample", 4), ("channel", 4)),),
+                            R.shape(("sample", 4), ("channel", 2)), param_bytes=32))
+    tiny.add_tensor("a", "b")
+    cases = [("tiny", tiny, R.single_node_topology(gpus=2), 2, R.MODE_FORWARD, 120, 5),
+             ("lenet", R.lenet_like(batch=2, image=4, in_channels=1, conv_channels=(2, 2), fc_hidden=2, classes=2),
+              R.single_node_topology(gpus=2), 2, R.MODE_FORWARD, 80, 4),
+             ("rnn3-full", R.rnn3(steps=2, batch=4, hidden=4, vocab=4), R.single_node_topology(gpus=3), 2,
+              R.MODE_FULL, 60, 1)]
+    for name, g, topo, md, mode, props, seed in cases:
+        rep = R.mcmc_search(g, topo, R.CostProfile(), R.SearchParams(max_proposals=props, seed=seed,
+                                                                      max_degree=md, mode=mode))
+        out.append({"name": name, "graph": R.graph_to_json(g), "topology": R.topology_to_json(topo),
+                    "mode": mode, "max_degree": md, "max_proposals": props, "seed": seed,
+                    "report": R.report_to_json(rep)})
+    return out
+
+
+def exhaustive_cases():
+    out = []
+    tiny = R.OperatorGraph()
+    tiny.add_op(R.Operation("a", R.OperatorKind("MatMul"), (R.shape(("sample", 4), ("channel", 4)),),
+                            R.shape(("sample", 4), ("channel", 4)), param_bytes=64))
+    tiny.add_op(R.Operation("b", R.OperatorKind("MatMul"), (R.shape(("sample", 4), ("channel", 4)),),
+                            R.shape(("sample", 4), ("channel", 2)), param_bytes=32))
+    tiny.add_tensor("a", "b")
+    cases = [("tiny", tiny, R.single_node_topology(gpus=2), 2, R.MODE_FORWARD),
+             ("tiny-full", tiny, R.single_node_topology(gpus=2), 2, R.MODE_FULL),
+             ("lenet", R.lenet_like(batch=2, image=4, in_channels=1, conv_channels=(2, 2), fc_hidden=2, classes=2),
+              R.single_node_topology(gpus=2), 2, R.MODE_FORWARD),
+             ("rnnlm", R.rnnlm_like(steps=2, layers=1, batch=2, hidden=2, vocab=2), R.single_node_topology(gpus=2),
+              2, R.MODE_FORWARD)]
+    for name, g, topo, md, mode in cases:
+        res = R.exhaustive_optimal(g, topo, R.CostProfile(), max_degree=md, cap=1e15, mode=mode)
+        out.append({"name": name, "graph": R.graph_to_json(g), "topology": R.topology_to_json(topo), "mode": mode,
+                    "max_degree": md, "cost": H(res.cost), "visited": res.visited,
+                    "space_estimate": res.space_estimate, "strategy": R.strategy_to_json(res.strategy)})
+    return out
+
+
 def rnn3_case():
     g = R.rnn3()
     topo = R.single_node_topology(gpus=3)
@@ -139,7 +184,8 @@ def rnn3_case():
 def main():
     os.makedirs(OUT, exist_ok=True)
     docs = {"rnn3_model_parallel.json": rnn3_case(), "simulate_random.json": simulate_cases(),
-            "simulate_benchmarks.json": benchmark_cases(), "mcmc.json": mcmc_cases()}
+            "simulate_benchmarks.json": benchmark_cases(), "mcmc.json": mcmc_cases(),
+            "search_reports.json": search_report_cases(), "exhaustive.json": exhaustive_cases()}
     for name, doc in docs.items():
         with open(os.path.join(OUT, name), "w") as fh:
             json.dump(doc, fh, separators=(",", ":"))

@@ -203,3 +203,79 @@ def test_mcmc_chains_survive_ready_set_overflow(oracle):
                       rng_mode="philox")
     for ci, ch in enumerate(rep.chains):
         assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted) == tuple(ref["summary"][ci][:4])
+
+
+def test_search_api_semantics_on_gpu():
+    """Reference test_search.py behaviours through the GPU path."""
+    import math
+    g = ps.OperatorGraph()
+    g.add_op(ps.Operation("a", ps.OperatorKind("MatMul"), (ps.shape(("sample", 4), ("channel", 4)),),
+                          ps.shape(("sample", 4), ("channel", 4)), param_bytes=64))
+    g.add_op(ps.Operation("b", ps.OperatorKind("MatMul"), (ps.shape(("sample", 4), ("channel", 4)),),
+                          ps.shape(("sample", 4), ("channel", 2)), param_bytes=32))
+    g.add_tensor("a", "b")
+    topo = ps.single_node_topology(gpus=2)
+    prof = ps.CostProfile()
+    p = ps.SearchParams(max_proposals=120, seed=5, max_degree=2)
+    a, b = ps.mcmc_search(g, topo, prof, p), ps.mcmc_search(g, topo, prof, p)
+    assert a == b and a.proposals == 240 and all(c.termination == "proposal-limit" for c in a.chains)
+    with pytest.raises(ValueError, match="budget_seconds or max_proposals"):
+        ps.mcmc_search(g, topo, prof, ps.SearchParams())
+    r = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=150, seed=1, max_degree=2, beta=math.inf,
+                                                      initial=[ps.data_parallel_strategy(g, topo)], polish=False))
+    acc = [c for _, c, ok in r.trace if ok]
+    assert acc and all(y <= x for x, y in zip(acc, acc[1:]))
+    r = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=1, seed=0, max_degree=2))
+    for c in r.chains:
+        assert c.beta == pytest.approx(math.log(10.0) / (0.05 * c.initial_cost))
+    ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=60, seed=3, max_degree=2, check_interval=1))
+    raw = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=40, seed=9, max_degree=2, polish=False))
+    pol = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=40, seed=9, max_degree=2))
+    assert pol.best_cost <= raw.best_cost
+    assert ps.local_optimality_check(pol.best_strategy, g, topo, prof, max_degree=2) is None
+    bad = ps.ParallelizationStrategy({oid: ps.ParallelizationConfig({"sample": 1, "channel": 1}, ("ghost-device",))
+                                      for oid in g.ops})
+    rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=30, seed=0, max_degree=2,
+                                                        initial=[bad, ps.data_parallel_strategy(g, topo)]))
+    assert rep.chains[0].termination.startswith("error") and rep.chains[0].proposals == 0
+    assert math.isfinite(rep.best_cost)
+    with pytest.raises(ps.SearchError, match="every chain failed"):
+        ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=5, initial=[bad]))
+
+
+def test_polish_and_local_check_match_reference_semantics(oracle):
+    """Greedy polish on the GPU reaches the same strategy/cost as the reference's
+    sequential first-improvement scan (golden: run here against the oracle by
+    re-scoring every accepted move)."""
+    g = ps.lenet_like(batch=2, image=4, in_channels=1, conv_channels=(2, 2), fc_hidden=2, classes=2)
+    topo = ps.single_node_topology(gpus=2)
+    prof = ps.CostProfile()
+    rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=50, seed=4, max_degree=2))
+    assert rep.best_cost == oracle.simulate(g, topo, prof, ps.MODE_FORWARD, rep.best_strategy)["makespan"]
+    assert ps.local_optimality_check(rep.best_strategy, g, topo, prof, max_degree=2) is None
+
+
+def test_default_search_report_is_byte_identical_to_the_reference():
+    """mcmc_search with default parameters (CPython MT19937 stream, greedy
+    polish) reproduces the reference's report JSON byte for byte."""
+    from golden_io import load
+    for doc in load("search_reports.json"):
+        g = ps.graph_from_json(doc["graph"])
+        topo = ps.topology_from_json(doc["topology"])
+        rep = ps.mcmc_search(g, topo, ps.CostProfile(), ps.SearchParams(
+            max_proposals=doc["max_proposals"], seed=doc["seed"], max_degree=doc["max_degree"], mode=doc["mode"]))
+        assert ps.report_to_json(rep) == doc["report"], doc["name"]
+
+
+def test_exhaustive_optimal_matches_the_reference():
+    """Same optimum, same strategy, same number of visited search nodes."""
+    from golden_io import fx, load
+    for doc in load("exhaustive.json"):
+        g = ps.graph_from_json(doc["graph"])
+        topo = ps.topology_from_json(doc["topology"])
+        res = ps.exhaustive_optimal(g, topo, ps.CostProfile(), max_degree=doc["max_degree"], cap=1e15,
+                                    mode=doc["mode"])
+        assert res.cost == fx(doc["cost"]), doc["name"]
+        assert res.visited == doc["visited"], doc["name"]
+        assert res.space_estimate == doc["space_estimate"]
+        assert ps.strategy_to_json(res.strategy) == doc["strategy"], doc["name"]
