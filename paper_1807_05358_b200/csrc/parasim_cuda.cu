@@ -230,28 +230,7 @@ __global__ void k_pack(DevProb P, int n_ent, void *ent16, void *cent16) {
 }
 
 // ---------------------------------------------------------------- simulator
-struct Scratch {
-  double *ready_f, *ready_b, *ready_g;
-  int *rem_f, *rem_b, *rem_g;
-  unsigned long long *gmask;
-};
 
-__host__ __device__ inline size_t scratch_bytes(int n_slots) {
-  size_t b = (size_t)n_slots * (3 * sizeof(double) + 3 * sizeof(int) + sizeof(unsigned long long));
-  return (b + 127) & ~(size_t)127;  // keep every warp's slice 128-byte aligned
-}
-
-__device__ inline Scratch scratch_at(char *base, int n_slots) {
-  Scratch s;
-  s.ready_f = (double *)base;
-  s.ready_b = s.ready_f + n_slots;
-  s.ready_g = s.ready_b + n_slots;
-  s.gmask = (unsigned long long *)(s.ready_g + n_slots);
-  s.rem_f = (int *)(s.gmask + n_slots);
-  s.rem_b = s.rem_f + n_slots;
-  s.rem_g = s.rem_b + n_slots;
-  return s;
-}
 
 struct WarpSmem {
   double *qclock;
@@ -259,18 +238,7 @@ struct WarpSmem {
   int *raux;
 };
 
-__host__ __device__ inline size_t warp_smem_bytes(int n_queues, int cap) {
-  return (size_t)n_queues * 8 + (size_t)cap * 20 + 16;
-}
 
-__device__ inline WarpSmem warp_smem_at(char *base, int n_queues, int cap) {
-  WarpSmem w;
-  w.qclock = (double *)base;
-  w.rhi = (unsigned long long *)(w.qclock + n_queues);
-  w.rlo = w.rhi + cap;
-  w.raux = (int *)(w.rlo + cap);
-  return w;
-}
 
 struct TraceSink {
   ps_trace_task *tasks;
@@ -324,286 +292,6 @@ __device__ __forceinline__ bool warp_push(bool want, double ready, unsigned long
   return true;
 }
 
-// Simulates one strategy with the calling warp.  map: [n_ops] local map
-// indices, asg: [n_slots] devices.  Exact replay of full_simulate.
-template <bool TRACE>
-__device__ SimOut warp_simulate(const DevProb &P, const int *__restrict__ map, const unsigned char *__restrict__ asg,
-                                const Scratch &S, const WarpSmem &w, int lane, const TraceSink *tr) {
-  SimOut out;
-  out.makespan = 0.0;
-  out.status = PS_STATUS_OK;
-  out.err_a = out.err_b = -1;
-  const int NF = P.n_slots;
-  for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = 0.0;
-  if (P.full)
-    for (int s = lane; s < NF; s += 32) S.gmask[s] = 0ull;
-  __syncwarp();
-  int n = 0;
-  bool okcap = true;
-  // ---- init: in-degrees, sources, ring membership
-  for (int base = 0; base < NF; base += 32) {
-    int s = base + lane;
-    bool want = false;
-    unsigned long long key = 0;
-    if (s < NF) {
-      int o = P.slot_op[s];
-      int k = s - P.op_slot_off[o];
-      int m = map[o];
-      int g = P.op_map_off[o] + m;
-      if (k < P.map_size[g]) {
-        int indeg = 0;
-        for (int i = P.op_in_off[o]; i < P.op_in_off[o + 1]; ++i) {
-          int p = P.op_in_pairs[i];
-          int sp = P.pair_src[p];
-          int nmd = P.op_map_off[o + 1] - P.op_map_off[o];
-          int c = P.combo_off[p] + map[sp] * nmd + m;
-          int col = P.combo_col_off[c] + k;
-          indeg += P.col_ent_off[col + 1] - P.col_ent_off[col];
-        }
-        S.rem_f[s] = indeg;
-        S.ready_f[s] = 0.0;
-        if (P.full) {
-          int outd = 1;
-          for (int i = P.op_out_off[o]; i < P.op_out_off[o + 1]; ++i) {
-            int p = P.op_out_pairs[i];
-            int dp = P.pair_dst[p];
-            int nmd = P.op_map_off[dp + 1] - P.op_map_off[dp];
-            int c = P.combo_off[p] + m * nmd + map[dp];
-            int row = P.combo_row_off[c] + k;
-            outd += P.row_ent_off[row + 1] - P.row_ent_off[row];
-          }
-          S.rem_b[s] = outd;
-          S.ready_b[s] = 0.0;
-          if (P.op_param_mask[o] >= 0) {
-            int si = group_of(P, o, g, k);
-            atomicOr(&S.gmask[P.op_slot_off[o] + si], 1ull << asg[s]);
-            // slot op_slot_off[o]+k doubles as the hop-0 counter of group k
-            if (k < P.map_ngroups[g]) {
-              S.rem_g[s] = P.map_size[g] / P.map_ngroups[g];
-              S.ready_g[s] = 0.0;
-            }
-          }
-        }
-        if (indeg == 0) {
-          want = true;
-          key = pack_key(KIND_OP, o, 0, k, 0);
-        }
-      }
-    }
-    okcap &= warp_push(want, 0.0, key, s, n, P.cap, w, lane);
-  }
-  __syncwarp();
-  if (!okcap) { out.status = PS_STATUS_CAPACITY; return out; }
-  int popped = 0;
-  // ---- event loop: pop the global minimum (ready, origin), as heapq does
-  while (n > 0) {
-    unsigned long long bh = ~0ull, bl = ~0ull;
-    int bp = 0;
-    for (int i = lane; i < n; i += 32) {
-      unsigned long long h = w.rhi[i], l = w.rlo[i];
-      if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; bp = i; }
-    }
-    unsigned cand = FULLMASK;
-    unsigned v, mn;
-    v = (unsigned)(bh >> 32); mn = __reduce_min_sync(FULLMASK, v); cand = __ballot_sync(FULLMASK, v == mn);
-    v = (cand >> lane & 1) ? (unsigned)bh : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
-    cand &= __ballot_sync(FULLMASK, v == mn);
-    v = (cand >> lane & 1) ? (unsigned)(bl >> 32) : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
-    cand &= __ballot_sync(FULLMASK, v == mn);
-    v = (cand >> lane & 1) ? (unsigned)bl : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
-    cand &= __ballot_sync(FULLMASK, v == mn);
-    int win = __ffs(cand) - 1;
-    int pos = __shfl_sync(FULLMASK, bp, win);
-    unsigned long long key = w.rlo[pos];
-    double ready = __longlong_as_double((long long)w.rhi[pos]);
-    int aux = w.raux[pos];
-    __syncwarp();
-    if (lane == 0) {
-      w.rhi[pos] = w.rhi[n - 1];
-      w.rlo[pos] = w.rlo[n - 1];
-      w.raux[pos] = w.raux[n - 1];
-    }
-    --n;
-    __syncwarp();
-    // ---- decode the task: queue and exe time
-    unsigned kind = key_kind(key), a = key_a(key), b = key_b(key), c = key_c(key), d = key_d(key);
-    int q;
-    double exe, nbytes = 0.0;
-    int ring_r = 0;
-    if (kind == KIND_OP || kind == KIND_OP_BWD) {
-      int o = a;
-      int dev = asg[P.op_slot_off[o] + c];
-      q = dev;
-      int g = P.op_map_off[o] + map[o];
-      exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[g * P.n_kinds + P.dev_kind[dev]];
-    } else if (kind == KIND_SYNC) {
-      int o = a;
-      int g = P.op_map_off[o] + map[o];
-      unsigned long long msk = S.gmask[P.op_slot_off[o] + b];
-      ring_r = __popcll((long long)msk);
-      int da = nth_bit(msk, c % ring_r), db = nth_bit(msk, (c + 1) % ring_r);
-      int li = P.link_of[da * P.n_dev + db];
-      if (li < 0) { out.status = PS_STATUS_NO_ROUTE; out.err_a = da; out.err_b = db; return out; }
-      q = P.n_dev + li;
-      nbytes = P.map_shard[g] / (double)ring_r;
-      exe = P.link_lat[li] + nbytes / P.link_bw[li];
-    } else {
-      int da = asg[P.op_slot_off[a] + c], db = asg[P.op_slot_off[b] + d];
-      int li = P.link_of[da * P.n_dev + db];
-      if (li < 0) { out.status = PS_STATUS_NO_ROUTE; out.err_a = da; out.err_b = db; return out; }
-      q = P.n_dev + li;
-      long long bytes = P.ent_bytes[aux];
-      nbytes = (double)bytes;
-      exe = P.link_lat[li] + nbytes / P.link_bw[li];
-    }
-    double clk = w.qclock[q];
-    double start = ready < clk ? clk : ready;
-    double end = start + exe;
-    __syncwarp();
-    if (lane == 0) w.qclock[q] = end;
-    if (end > out.makespan) out.makespan = end;
-    int my_index = popped++;
-    if (TRACE && lane == 0) {
-      int t = atomicAdd(tr->n_tasks, 1);
-      if (t < tr->task_cap) {
-        ps_trace_task r;
-        r.key = key; r.queue = q; r.aux = aux; r.exe = exe; r.nbytes = nbytes;
-        r.ready = ready; r.start = start; r.end = end;
-        tr->tasks[t] = r;
-      }
-    }
-    // ---- relax successors
-    bool want = false;
-    unsigned long long skey = 0;
-    double sready = 0.0;
-    int saux = 0;
-#define EMIT_EDGE(succkey)                                          \
-  if (TRACE) {                                                      \
-    int e_ = atomicAdd(tr->n_edges, 1);                             \
-    if (e_ < tr->edge_cap) { tr->edge_pred[e_] = my_index; tr->edge_succ[e_] = (succkey); } \
-  }
-    if (kind == KIND_OP) {
-      int o = a, k = c, m = map[o];
-      int dev = asg[P.op_slot_off[o] + k];
-      if (P.full) {
-        int s = P.op_slot_off[o] + k;
-        want = false;
-        sready = 0.0;
-        if (lane == 0) {
-          double r = S.ready_b[s];
-          if (end > r) { r = end; S.ready_b[s] = r; }
-          EMIT_EDGE(pack_key(KIND_OP_BWD, o, 0, k, 0));
-          if (--S.rem_b[s] == 0) { want = true; sready = r; }
-        }
-        if (!warp_push(want, sready, pack_key(KIND_OP_BWD, o, 0, k, 0), s, n, P.cap, w, lane)) goto overflow;
-      }
-      for (int i = P.op_out_off[o]; i < P.op_out_off[o + 1]; ++i) {
-        int p = P.op_out_pairs[i];
-        int dp = P.pair_dst[p];
-        int nmd = P.op_map_off[dp + 1] - P.op_map_off[dp];
-        int cc = P.combo_off[p] + m * nmd + map[dp];
-        int row = P.combo_row_off[cc] + k;
-        int e0 = P.row_ent_off[row], e1 = P.row_ent_off[row + 1];
-        for (int eb = e0; eb < e1; eb += 32) {
-          int e = eb + lane;
-          want = false;
-          if (e < e1) {
-            int l = P.ent_l[e];
-            int ds = P.op_slot_off[dp] + l;
-            int ddev = asg[ds];
-            if (ddev == dev) {
-              double r = S.ready_f[ds];
-              if (end > r) { r = end; S.ready_f[ds] = r; }
-              EMIT_EDGE(pack_key(KIND_OP, dp, 0, l, 0));
-              if (--S.rem_f[ds] == 0) { want = true; sready = r; skey = pack_key(KIND_OP, dp, 0, l, 0); saux = ds; }
-            } else {
-              // link existence is checked when the transfer is dequeued
-              skey = pack_key(KIND_EDGE, o, dp, k, l);
-              EMIT_EDGE(skey);
-              want = true; sready = end; saux = e;
-            }
-          }
-          if (!warp_push(want, sready, skey, saux, n, P.cap, w, lane)) goto overflow;
-        }
-      }
-    } else if (kind == KIND_EDGE || kind == KIND_EDGE_BWD) {
-      // edge: -> op(d, l);  edge_bwd: -> op_bwd(s, k)
-      int o = kind == KIND_EDGE ? b : a;
-      int k = kind == KIND_EDGE ? d : c;
-      int s = P.op_slot_off[o] + k;
-      double *rd = kind == KIND_EDGE ? S.ready_f : S.ready_b;
-      int *rm = kind == KIND_EDGE ? S.rem_f : S.rem_b;
-      unsigned long long sk = pack_key(kind == KIND_EDGE ? KIND_OP : KIND_OP_BWD, o, 0, k, 0);
-      want = false;
-      if (lane == 0) {
-        double r = rd[s];
-        if (end > r) { r = end; rd[s] = r; }
-        EMIT_EDGE(sk);
-        if (--rm[s] == 0) { want = true; sready = r; }
-      }
-      if (!warp_push(want, sready, sk, s, n, P.cap, w, lane)) goto overflow;
-    } else if (kind == KIND_OP_BWD) {
-      int o = a, k = c, m = map[o];
-      int dev = asg[P.op_slot_off[o] + k];
-      int nmo = P.op_map_off[o + 1] - P.op_map_off[o];
-      for (int i = P.op_in_off[o]; i < P.op_in_off[o + 1]; ++i) {
-        int p = P.op_in_pairs[i];
-        int sp = P.pair_src[p];
-        int cc = P.combo_off[p] + map[sp] * nmo + m;
-        int col = P.combo_col_off[cc] + k;
-        int j0 = P.col_ent_off[col], j1 = P.col_ent_off[col + 1];
-        for (int jb = j0; jb < j1; jb += 32) {
-          int j = jb + lane;
-          want = false;
-          if (j < j1) {
-            int e = P.col_ent[j];
-            int kk = P.ent_k[e];
-            int ss = P.op_slot_off[sp] + kk;
-            int sdev = asg[ss];
-            if (sdev == dev) {
-              double r = S.ready_b[ss];
-              if (end > r) { r = end; S.ready_b[ss] = r; }
-              EMIT_EDGE(pack_key(KIND_OP_BWD, sp, 0, kk, 0));
-              if (--S.rem_b[ss] == 0) { want = true; sready = r; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); saux = ss; }
-            } else {
-              // the forward pass already proved this link exists
-              skey = pack_key(KIND_EDGE_BWD, sp, o, kk, k);
-              EMIT_EDGE(skey);
-              want = true; sready = end; saux = e;
-            }
-          }
-          if (!warp_push(want, sready, skey, saux, n, P.cap, w, lane)) goto overflow;
-        }
-      }
-      if (P.op_param_mask[o] >= 0) {
-        int g = P.op_map_off[o] + m;
-        int si = group_of(P, o, g, k);
-        int gs = P.op_slot_off[o] + si;
-        unsigned long long msk = S.gmask[gs];
-        want = false;
-        sready = 0.0;
-        if (__popcll((long long)msk) >= 2 && lane == 0) {
-          double r = S.ready_g[gs];
-          if (end > r) { r = end; S.ready_g[gs] = r; }
-          EMIT_EDGE(pack_key(KIND_SYNC, o, si, 0, 0));
-          if (--S.rem_g[gs] == 0) { want = true; sready = r; }
-        }
-        if (!warp_push(want, sready, pack_key(KIND_SYNC, o, si, 0, 0), gs, n, P.cap, w, lane)) goto overflow;
-      }
-    } else {  // KIND_SYNC: chain to the next hop of the ring
-      want = lane == 0 && (int)c + 1 < 2 * (ring_r - 1);
-      if (want) EMIT_EDGE(pack_key(KIND_SYNC, a, b, c + 1, 0));
-      if (!warp_push(want, end, pack_key(KIND_SYNC, a, b, c + 1, 0), aux, n, P.cap, w, lane)) goto overflow;
-    }
-    __syncwarp();
-  }
-#undef EMIT_EDGE
-  return out;
-overflow:
-  out.status = PS_STATUS_CAPACITY;
-  return out;
-}
-
 // ================================================================ v2 simulator
 // Latency-optimised replay used by k_simulate_batch and k_mcmc.
 //
@@ -632,8 +320,9 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 struct Tab {  // block-shared copies of small static tables
   int *op_slot_off, *op_map_off, *op_in_off, *op_in_pairs, *op_out_off, *op_out_pairs, *op_param_mask;
-  int *pair_src, *pair_dst, *combo_off, *dev_kind, *link_of;
-  double *link_lat, *link_bw;
+  int *pair_src, *pair_dst, *combo_off, *dev_kind;
+  short *link_of;                      // device pair -> link index (-1: none)
+  const double *link_lat, *link_bw;    // global, read-only path
 };
 
 struct Lay {  // sizes shared by host and device
@@ -641,6 +330,7 @@ struct Lay {  // sizes shared by host and device
   int SC;  // dense counter capacity (fwd + bwd + ring counters) kept in shared memory
   int GC;  // parameter-shard (ring) capacity
   int RC;  // staged row / column offset capacity
+  int asg_global;  // device assignment read in place from global memory (very wide problems)
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -650,21 +340,20 @@ __host__ __device__ inline size_t tab_bytes_of(const DevProb &P) {
   b += al16(4 * (size_t)(P.n_ops + 1)) * 4;          // slot_off, map_off, in_off, out_off
   b += al16(4 * (size_t)(P.n_pairs + 1)) * 5;        // in_pairs, out_pairs, src, dst, combo_off
   b += al16(4 * (size_t)P.n_ops);                    // param mask
-  b += al16(4 * (size_t)P.n_dev) + al16(4 * (size_t)P.n_dev * P.n_dev);
-  b += al16(8 * (size_t)(P.n_links + 1)) * 2;
+  b += al16(4 * (size_t)P.n_dev) + al16(2 * (size_t)P.n_dev * P.n_dev);
   return b;
 }
 
-__host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC, int RC) {
+__host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC, int RC, int asg_global = 0) {
   size_t b = 0;
   b += al16(4 * (size_t)P.n_ops) * 2;                // mapl, gmap
   b += al16(4 * (size_t)(P.n_ops + 1)) * 2;          // fbase, gbase
   b += al16(4 * (size_t)P.n_pairs) * 2;              // prow, pcol
-  b += al16((size_t)P.n_slots);                      // asg
+  b += asg_global ? 0 : al16((size_t)P.n_slots);     // asg
   b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
   b += al16(8 * (size_t)P.n_ops) + 16 + 128;         // per-op forward exe cache, flags, winner lanes
-  b += al16(4 * (size_t)P.n_queues);                 // queue claims
+  b += 4 * 256;                                      // queue claims (hashed)
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
@@ -685,6 +374,7 @@ struct W2 {
   int *qown;   // [Q] last member to claim the queue this round
   int rcap;    // ready-set capacity in effect (shared memory, or the global overflow slice)
   double *opmin;  // optional [n_ops]: earliest end of each op's forward tasks (exhaustive bounds)
+  const TraceSink *tr;  // optional: record every task and dependency (API materialisation)
   double *cready;
   unsigned short *crem;
   unsigned char *cgrp;
@@ -708,9 +398,9 @@ __device__ inline void carve_tab(char *base, const DevProb &P, Tab &t) {
   t.combo_off = (int *)take(4 * (P.n_pairs + 1));
   t.op_param_mask = (int *)take(4 * P.n_ops);
   t.dev_kind = (int *)take(4 * P.n_dev);
-  t.link_of = (int *)take(4 * P.n_dev * P.n_dev);
-  t.link_lat = (double *)take(8 * (P.n_links + 1));
-  t.link_bw = (double *)take(8 * (P.n_links + 1));
+  t.link_of = (short *)take(2 * P.n_dev * P.n_dev);
+  t.link_lat = P.link_lat;
+  t.link_bw = P.link_bw;
 }
 
 __device__ inline void load_tab(const DevProb &P, const Tab &t) {
@@ -728,8 +418,7 @@ __device__ inline void load_tab(const DevProb &P, const Tab &t) {
   for (int i = tid; i <= P.n_pairs; i += nt) t.combo_off[i] = P.combo_off[i];
   for (int i = tid; i < P.n_ops; i += nt) t.op_param_mask[i] = P.op_param_mask[i];
   for (int i = tid; i < P.n_dev; i += nt) t.dev_kind[i] = P.dev_kind[i];
-  for (int i = tid; i < P.n_dev * P.n_dev; i += nt) t.link_of[i] = P.link_of[i];
-  for (int i = tid; i < P.n_links; i += nt) { t.link_lat[i] = P.link_lat[i]; t.link_bw[i] = P.link_bw[i]; }
+  for (int i = tid; i < P.n_dev * P.n_dev; i += nt) t.link_of[i] = (short)P.link_of[i];
 }
 
 __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2 &w) {
@@ -741,7 +430,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.gbase = (int *)take(4 * (P.n_ops + 1));
   w.prow = (int *)take(4 * P.n_pairs);
   w.pcol = (int *)take(4 * P.n_pairs);
-  w.asg = (unsigned char *)take(P.n_slots);
+  w.asg = L.asg_global ? nullptr : (unsigned char *)take(P.n_slots);
   w.qclock = (double *)take(8 * P.n_queues);
   w.rhi = (unsigned long long *)take(8 * P.cap);
   w.rlo = (unsigned long long *)take(8 * P.cap);
@@ -751,7 +440,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.exef = (double *)take(8 * P.n_ops);
   w.flags = (int *)take(16);
   w.wlane = (int *)take(128);
-  w.qown = (int *)take(4 * P.n_queues);
+  w.qown = (int *)take(4 * 256);
   w.cready = (double *)take(8 * L.SC);
   w.crem = (unsigned short *)take(2 * L.SC);
   w.cgrp = (unsigned char *)take(L.SC);
@@ -762,6 +451,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.ph = (unsigned long long *)take(128);
   w.rcap = P.cap;
   w.opmin = nullptr;
+  w.tr = nullptr;
 }
 
 struct State {  // one candidate's dense counters (shared memory, or a global slice)
@@ -960,7 +650,7 @@ __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int d
   int li = T.link_of[da * P.n_dev + db];
   if (li < 0) return false;
   q = P.n_dev + li;
-  exe = T.link_lat[li] + nb / T.link_bw[li];
+  exe = __ldg(&T.link_lat[li]) + nb / __ldg(&T.link_bw[li]);
   return true;
 }
 
@@ -993,6 +683,27 @@ __device__ unsigned long long g_phase[16];
 #define PH_ADD(i, t0)
 #define PH_CNT(i, x)
 #endif
+
+// Transfer bytes of an edge task from its key (trace mode only): row k of the
+// pair's current combo, searched for column l.
+__device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &w, const State &st,
+                                      unsigned long long key) {
+  unsigned kind = key_kind(key);
+  int a = key_a(key), b = key_b(key), c = key_c(key), d = key_d(key);
+  if (kind == KIND_SYNC) {
+    unsigned long long msk = st.gmask[w.gbase[a] + b];
+    return P.map_shard[w.gmap[a]] / (double)__popcll((long long)msk);
+  }
+  if (kind != KIND_EDGE && kind != KIND_EDGE_BWD) return 0.0;
+  for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
+    int p = T.op_out_pairs[i];
+    if (T.pair_dst[p] != b) continue;
+    int row = w.prow[p] + c;
+    for (int e = st.rowoff[row]; e < st.rowoff[row + 1]; ++e)
+      if ((int)P.ent_l[e] == d) return (double)P.ent_bytes[e];
+  }
+  return 0.0;
+}
 
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   SimOut out;
@@ -1083,7 +794,6 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     PH_T(t_sel);
     PH_CNT(11, 1);
     PH_CNT(12, n);
-    unsigned wbits = 0;  // lanes holding this round's winners
     bool mine = false;
     int nw = 0;
     unsigned long long mykey = 0;
@@ -1107,9 +817,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // per-queue minimum (ready, origin) among members: each member claims its
       // queue; a member alone on its queue wins outright, and only queues claimed
       // twice take a group-restricted lexicographic min
-      if (member) w.qown[q] = lane;
+      if (member) w.qown[q & 255] = lane;
       __syncwarp();
-      bool lost = member && w.qown[q] != lane;
+      bool lost = member && w.qown[q & 255] != lane;
       bool win = member;
       if (__any_sync(FULLMASK, lost)) {
       unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
@@ -1135,7 +845,6 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = q;
       }
       n = __popc(kb);
-      wbits = wb;
       mine = win;
       if (win) w.wlane[__popc(wb & ((1u << lane) - 1u))] = lane;
       mykey = k; myready = r; myexe = e; myq = q;
@@ -1225,19 +934,30 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         __syncwarp();
       }
       mine = lane < nw;
-      wbits = nw == 32 ? FULLMASK : ((1u << nw) - 1u);
       w.wlane[lane] = lane;
     }
     // ---- run the winners: distinct queues, each its queue's next task
-    double end = 0.0;
+    double end = 0.0, mystart = 0.0;
     if (mine) {
       double clk = w.qclock[myq];
       double start = myready < clk ? clk : myready;
+      mystart = start;
       end = start + myexe;
       w.qclock[myq] = end;
       if (end > out.makespan) out.makespan = end;
       if (w.opmin && key_kind(mykey) == KIND_OP)
         atomicMin((unsigned long long *)&w.opmin[key_a(mykey)], (unsigned long long)__double_as_longlong(end));
+    }
+    int myrec = -1;
+    if (w.tr && mine) {
+      myrec = atomicAdd(w.tr->n_tasks, 1);
+      if (myrec < w.tr->task_cap) {
+        ps_trace_task rec;
+        rec.key = mykey; rec.queue = myq; rec.aux = 0; rec.exe = myexe;
+        rec.nbytes = trace_nbytes(P, T, w, st, mykey);
+        rec.ready = myready; rec.start = mystart; rec.end = end;
+        w.tr->tasks[myrec] = rec;
+      }
     }
     PH_ADD(2, t_sel);
     PH_CNT(13, nw);
@@ -1252,6 +972,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int srcl = act_lane ? w.wlane[wi] : 0;
     unsigned long long wkey = __shfl_sync(FULLMASK, mykey, srcl);
     double wend = __shfl_sync(FULLMASK, end, srcl);
+    int wrec = __shfl_sync(FULLMASK, myrec, srcl);
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
     int wdev = 0, head = 0, tail = 0, L = 0, ring = 0;
     int fe = -1, fp = 0;  // this lane's first list entry (index j0) and its pair
@@ -1376,6 +1097,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           if (!sync_attrs(P, T, w, st, a, b, c + 1, pq, pexe, ea, eb)) err = true;
         }
       }
+      if (w.tr && act != 0 && wrec >= 0) {
+        int e_ = atomicAdd(w.tr->n_edges, 1);
+        if (e_ < w.tr->edge_cap) { w.tr->edge_pred[e_] = wrec; w.tr->edge_succ[e_] = skey; }
+      }
       // arrivals: every max lands before any count reaches zero (the warp
       // barrier orders them); the u16 counter is decremented through the
       // 32-bit word that holds it (no borrow: it stops at zero)
@@ -1442,7 +1167,9 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
     const int *m = maps + (size_t)cand * P.n_ops;
     const unsigned char *a = asgs + (size_t)cand * P.n_slots;
     for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = m[i];
-    for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = a[i];
+    if (lay.asg_global) w.asg = const_cast<unsigned char *>(a);
+    else
+      for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = a[i];
     if (opmin) {
       w.opmin = opmin + (size_t)cand * P.n_ops;
       for (int i = lane; i < P.n_ops; i += 32) w.opmin[i] = __longlong_as_double(0x7ff0000000000000ll);
@@ -1458,13 +1185,30 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
 }
 
 __global__ void __launch_bounds__(32)
-k_simulate_trace(DevProb P, const int *map, const unsigned char *asg, char *scratch, TraceSink tr,
+k_simulate_trace(DevProb P, Lay lay, const int *map, const unsigned char *asg, char *gscratch, TraceSink tr,
                  double *makespan, int *status, int *err) {
   extern __shared__ __align__(16) char smem[];
+  Tab T;
+  carve_tab(smem, P, T);
+  load_tab(P, T);
+  __syncthreads();
   int lane = threadIdx.x & 31;
-  WarpSmem w = warp_smem_at(smem, P.n_queues, P.cap);
-  Scratch S = scratch_at(scratch, P.n_slots);
-  SimOut o = warp_simulate<true>(P, map, asg, S, w, lane, &tr);
+  W2 w;
+  carve_warp(smem + lay.tab_bytes, P, lay, w);
+  bind_bids(P, gscratch, w);
+  if (lane == 0) w.flags[0] = 1;
+  for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = map[i];
+  if (lay.asg_global) w.asg = const_cast<unsigned char *>(asg);
+  else
+    for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = asg[i];
+  w.tr = &tr;
+  __syncwarp();
+  SimOut o = warp_simulate2(P, T, w, lay, gscratch, lane);
+  if (o.status == PS_STATUS_CAPACITY) {  // wide ready set: rerun in global memory, fresh trace
+    if (lane == 0) { *tr.n_tasks = 0; *tr.n_edges = 0; }
+    __syncwarp();
+    o = warp_simulate2(P, T, with_global_ready_set(P, gscratch, w), lay, gscratch, lane);
+  }
   if (lane == 0) {
     *makespan = o.makespan;
     *status = o.status;
@@ -1473,10 +1217,6 @@ k_simulate_trace(DevProb P, const int *map, const unsigned char *asg, char *scra
   }
 }
 
-
-// Explicit task graph (hand-built TaskGraphs, and the oracle_simulate path):
-// one warp replays the (ready, origin-rank) heap order over CSR successors.
-// The ready set lives in global memory (capacity n_tasks).
 __global__ void __launch_bounds__(32)
 k_simulate_explicit(int n_tasks, int n_queues, const int *__restrict__ queue, const double *__restrict__ exe,
                     const unsigned long long *__restrict__ rank, const int *__restrict__ succ_off,
@@ -1651,7 +1391,9 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   ChainState cs = st[chain];
   if (cs.status != PS_STATUS_OK) return;
   for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = gmapl[i];
-  for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = gasg[i];
+  if (lay.asg_global) w.asg = gasg;
+  else
+    for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = gasg[i];
   __syncwarp();
   WarpRng rng;
   rng.mode = rng_mode;
@@ -1754,7 +1496,8 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   if (lane < 16) atomicAdd(&g_phase[lane], w.ph[lane]);
 #endif
   for (int i = lane; i < P.n_ops; i += 32) gmapl[i] = w.mapl[i];
-  for (int i = lane; i < P.n_slots; i += 32) gasg[i] = w.asg[i];
+  if (!lay.asg_global)
+    for (int i = lane; i < P.n_slots; i += 32) gasg[i] = w.asg[i];
   cs.key = rng.key;
   cs.ctr = rng.ctr;
   cs.bpos = rng.bpos;
@@ -1967,32 +1710,36 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
     size_t tb = al16(tab_bytes_of(P));
     int target = 7;  // 7 x 148 SMs = 1036 resident chains >= the 1024-chain workload
     if (const char *e = getenv("PS_TARGET_WARPS_PER_SM")) target = std::max(1, atoi(e));
-    int bestSC = -1, bestW = 0, bestWarps = 0, bestRC = 0, bestGC = 0;
+    int bestSC = -1, bestW = 0, bestWarps = 0, bestRC = 0, bestGC = 0, bestAG = 0;
     const int caps[] = {4096, 3072, 2048, 1536, 1280, 1024, 896, 768, 640, 512, 384, 256, 128, 0};
-    for (int ci = 0; ci < (int)(sizeof caps / sizeof caps[0]); ++ci) {
-      int SC = caps[ci];
-      int GC = std::max(16, SC / 4);
-      int RC = std::max(64, 3 * SC / 4);
-      size_t wb = al16(warp_bytes_of(P, SC, GC, RC));
-      int cw = 0, cwp = 0;
-      for (int wp : {8, 7, 6, 5, 4, 3, 2, 1}) {
-        size_t blk = tb + wp * wb;
-        if (blk > (size_t)optin) continue;
-        int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
-        int warps = std::min(64, blocks * wp);
-        if (warps > cw) { cw = warps; cwp = wp; }
+    int ag0 = getenv("PS_FORCE_ASG_GLOBAL") ? 1 : 0;  // test hook: exercise the in-place path
+    for (int ag = ag0; ag < 2 && bestWarps < target; ++ag) {
+      for (int ci = 0; ci < (int)(sizeof caps / sizeof caps[0]); ++ci) {
+        int SC = caps[ci];
+        int GC = std::max(16, SC / 4);
+        int RC = std::max(64, 3 * SC / 4);
+        size_t wb = al16(warp_bytes_of(P, SC, GC, RC, ag));
+        int cw = 0, cwp = 0;
+        for (int wp : {8, 7, 6, 5, 4, 3, 2, 1}) {
+          size_t blk = tb + wp * wb;
+          if (blk > (size_t)optin) continue;
+          int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
+          int warps = std::min(64, blocks * wp);
+          if (warps > cw) { cw = warps; cwp = wp; }
+        }
+        if (cw > bestWarps || (cw >= target && bestWarps < target)) {
+          bestWarps = cw; bestSC = SC; bestW = cwp; bestRC = RC; bestGC = GC; bestAG = ag;
+        }
+        if (cw >= target) break;
       }
-      if (cw > bestWarps || (cw >= target && bestWarps < target)) {
-        bestWarps = cw; bestSC = SC; bestW = cwp; bestRC = RC; bestGC = GC;
-      }
-      if (cw >= target) break;
     }
     if (bestSC < 0) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "problem too large for shared memory"); }
     pr->lay.tab_bytes = tb;
     pr->lay.SC = bestSC;
     pr->lay.GC = bestGC;
     pr->lay.RC = bestRC;
-    pr->lay.warp_bytes = al16(warp_bytes_of(P, bestSC, bestGC, bestRC));
+    pr->lay.asg_global = bestAG;
+    pr->lay.warp_bytes = al16(warp_bytes_of(P, bestSC, bestGC, bestRC, bestAG));
     pr->wpb = bestW;
     pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
     pr->blocks_per_sm = std::max(1, bestWarps / bestW);
@@ -2001,8 +1748,6 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   // problems with different layouts can coexist
   CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  size_t wsm = (warp_smem_bytes(P.n_queues, P.cap) + 15) & ~(size_t)15;
-  if (wsm > (size_t)optin) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "ready set too large for tracing"); }
   CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch, pr->wpb * 32, pr->smem_per_block));
@@ -2130,7 +1875,7 @@ int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   unsigned long long *des = nullptr;
   int *cnts = nullptr, *err = nullptr;
   double *dmk = nullptr;
-  CK(cudaMalloc(&scr, scratch_bytes(pr->P.n_slots)));
+  CK(cudaMalloc(&scr, gscratch_bytes(pr->P.n_slots, pr->P.n_queues)));
   CK(cudaMalloc(&dt, sizeof(ps_trace_task) * (size_t)std::max(task_cap, 1)));
   CK(cudaMalloc(&dep, sizeof(int32_t) * (size_t)std::max(edge_cap, 1)));
   CK(cudaMalloc(&des, sizeof(unsigned long long) * (size_t)std::max(edge_cap, 1)));
@@ -2143,8 +1888,8 @@ int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   TraceSink tr;
   tr.tasks = dt; tr.task_cap = task_cap; tr.n_tasks = cnts; tr.edge_pred = dep; tr.edge_succ = des;
   tr.edge_cap = edge_cap; tr.n_edges = cnts + 1;
-  size_t wsm = (warp_smem_bytes(pr->P.n_queues, pr->P.cap) + 15) & ~(size_t)15;
-  k_simulate_trace<<<1, 32, wsm>>>(pr->P, pr->d_map, pr->d_asg, scr, tr, dmk, err + 2, err);
+  size_t smem = pr->lay.tab_bytes + pr->lay.warp_bytes;
+  k_simulate_trace<<<1, 32, smem>>>(pr->P, pr->lay, pr->d_map, pr->d_asg, scr, tr, dmk, err + 2, err);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   int h[2], he[3];

@@ -279,3 +279,20 @@ def test_exhaustive_optimal_matches_the_reference():
         assert res.visited == doc["visited"], doc["name"]
         assert res.space_estimate == doc["space_estimate"]
         assert ps.strategy_to_json(res.strategy) == doc["strategy"], doc["name"]
+
+
+def test_in_place_global_assignment_layout(oracle, monkeypatch):
+    """Very wide problems keep device assignments in global memory; force that
+    layout on a small problem and check batch evaluation and MCMC parity."""
+    monkeypatch.setenv("PS_FORCE_ASG_GLOBAL", "1")
+    g, topo, mode, md = _random_case(4242)
+    prof = ps.CostProfile()
+    strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, s) for s in range(6)]
+    got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=md)
+    assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies))
+    init = strategies[:3]
+    rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=80, seed=7, max_degree=md, mode=mode,
+                                                        initial=init, polish=False, rng="philox"))
+    ref = oracle.mcmc(g, topo, prof, mode, init, [7 + 1000003 * c for c in range(3)], 80, md, rng_mode="philox")
+    for ci, ch in enumerate(rep.chains):
+        assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted) == tuple(ref["summary"][ci][:4])
