@@ -256,19 +256,6 @@ struct SimOut {
   int err_a, err_b;
 };
 
-__device__ __forceinline__ int group_of(const DevProb &P, int op, int g, int k) {
-  int nd = P.op_ndim[op], pm = P.op_param_mask[op];
-  int coords[PS_MAXDIM];
-  for (int i = nd - 1; i >= 0; --i) {
-    int d = P.map_deg[g * PS_MAXDIM + i];
-    coords[i] = k % d;
-    k /= d;
-  }
-  int si = 0;
-  for (int i = 0; i < nd; ++i)
-    if (pm >> i & 1) si = si * P.map_deg[g * PS_MAXDIM + i] + coords[i];
-  return si;
-}
 
 __device__ __forceinline__ int nth_bit(unsigned long long m, int n) {
   for (int i = 0; i < n; ++i) m &= m - 1;
