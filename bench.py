@@ -48,12 +48,13 @@ def parse():
                     help="time-boxed steps: each chain proposes until this much device time has passed")
     ap.add_argument("--mode", default="full-iteration", choices=("forward", "full-iteration"))
     ap.add_argument("--config", default="inception", choices=("inception", "alexnet", "resnet", "nmt", "random"))
+    ap.add_argument("--ops", type=int, default=1000, help="operator count of the random-DAG config")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
 
-def workload(name):
+def workload(name, ops=1000):
     import paper_1807_05358_b200 as ps
     if name == "inception":
         return ps.inception_v3(), ps.multi_node_topology(4, 4), 4, "Inception-v3 b64 on 4x4 GPUs (16 devices, 120 links)"
@@ -64,7 +65,7 @@ def workload(name):
     if name == "nmt":
         return (ps.nmt_like(steps=40, layers=2, batch=64, hidden=1024, vocab=32768), ps.multi_node_topology(16, 4), 8,
                 "NMT-40 on 16x4 GPUs")
-    return ps.random_dag(1000, seed=1000), ps.multi_node_topology(4, 4), 4, "random DAG 1k ops on 4x4 GPUs"
+    return ps.random_dag(ops, seed=1000), ps.multi_node_topology(4, 4), 4, f"random DAG {ops} ops on 4x4 GPUs"
 
 
 def initial_strategies(g, topo, md, first, count):
@@ -162,7 +163,7 @@ def run_reference(args):
     if rank != 0:
         return
     import paper_1807_05358_b200 as ps
-    g, topo, md, desc = workload(args.config)
+    g, topo, md, desc = workload(args.config, args.ops)
     prof = ps.CostProfile()
     threads = os.cpu_count() or 1
     init = initial_strategies(g, topo, md, 0, threads)
@@ -197,7 +198,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    g, topo, md, desc = workload(args.config)
+    g, topo, md, desc = workload(args.config, args.ops)
     prof = ps.CostProfile()
     C = args.chains
     first = rank * C

@@ -71,6 +71,7 @@ struct DevProb {
   const long long *ent_bytes;
   const void *ent16, *cent16;  // packed (k | l << 16, bytes) rows and column-ordered copies
   double mult;                 // backward_multiplier (exe_bwd == exe_fwd * mult, one IEEE product)
+  const short *link16;         // 16-bit copy of link_of (block tables in global mode)
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
@@ -318,6 +319,7 @@ struct Lay {  // sizes shared by host and device
   int GC;  // parameter-shard (ring) capacity
   int RC;  // staged row / column offset capacity
   int asg_global;  // device assignment read in place from global memory (very wide problems)
+  int global_all;  // block tables and warp slices in global memory (problems too big for shared memory)
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -390,6 +392,23 @@ __device__ inline void carve_tab(char *base, const DevProb &P, Tab &t) {
   t.link_bw = P.link_bw;
 }
 
+__device__ inline void tab_from_global(const DevProb &P, Tab &t) {
+  t.op_slot_off = const_cast<int *>(P.op_slot_off);
+  t.op_map_off = const_cast<int *>(P.op_map_off);
+  t.op_in_off = const_cast<int *>(P.op_in_off);
+  t.op_out_off = const_cast<int *>(P.op_out_off);
+  t.op_in_pairs = const_cast<int *>(P.op_in_pairs);
+  t.op_out_pairs = const_cast<int *>(P.op_out_pairs);
+  t.pair_src = const_cast<int *>(P.pair_src);
+  t.pair_dst = const_cast<int *>(P.pair_dst);
+  t.combo_off = const_cast<int *>(P.combo_off);
+  t.op_param_mask = const_cast<int *>(P.op_param_mask);
+  t.dev_kind = const_cast<int *>(P.dev_kind);
+  t.link_of = const_cast<short *>(P.link16);
+  t.link_lat = P.link_lat;
+  t.link_bw = P.link_bw;
+}
+
 __device__ inline void load_tab(const DevProb &P, const Tab &t) {
   int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i <= P.n_ops; i += nt) {
@@ -456,6 +475,25 @@ __host__ __device__ inline size_t gscratch_bytes(int n_slots, int n_queues) {
   return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 2) + al16((size_t)n_slots) +
          al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + (size_t)overflow_cap(n_slots) * 32 + 256;
 }
+
+// one warp's global slice: scratch, plus its whole shared-memory layout in global mode
+__host__ __device__ inline size_t gslice_bytes(const DevProb &P, const Lay &L) {
+  return al16(gscratch_bytes(P.n_slots, P.n_queues)) + (L.global_all ? L.warp_bytes : 0);
+}
+
+// prologue shared by the warp kernels: block tables and this warp's layout
+__device__ inline void kernel_layout(const DevProb &P, const Lay &L, char *smem, char *gslice, int wib, Tab &T,
+                                     W2 &w) {
+  if (L.global_all) {
+    tab_from_global(P, T);
+    carve_warp(gslice + al16(gscratch_bytes(P.n_slots, P.n_queues)), P, L, w);
+  } else {
+    carve_tab(smem, P, T);
+    load_tab(P, T);
+    carve_warp(smem + L.tab_bytes + wib * L.warp_bytes, P, L, w);
+  }
+}
+
 
 // slow-path per-queue bid arrays (ready bits, origin key): tail of the warp's global slice
 __device__ inline void bind_bids(const DevProb &P, char *gscratch, W2 &w) {
@@ -1138,15 +1176,13 @@ __global__ void __launch_bounds__(256, 1)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
                  double *makespan, int *status, char *gscratch, double *opmin) {
   extern __shared__ __align__(16) char smem[];
-  Tab T;
-  carve_tab(smem, P, T);
-  load_tab(P, T);
-  __syncthreads();
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  W2 w;
-  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay, w);
   int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
-  char *gs = gscratch + (size_t)gw * gscratch_bytes(P.n_slots, P.n_queues);
+  char *gs = gscratch + (size_t)gw * gslice_bytes(P, lay);
+  Tab T;
+  W2 w;
+  kernel_layout(P, lay, smem, gs, wib, T, w);
+  __syncthreads();
   bind_bids(P, gs, w);
   if (lane == 0) w.flags[0] = 1;  // the global bid arrays start uninitialised
   __syncwarp();
@@ -1175,13 +1211,11 @@ __global__ void __launch_bounds__(32)
 k_simulate_trace(DevProb P, Lay lay, const int *map, const unsigned char *asg, char *gscratch, TraceSink tr,
                  double *makespan, int *status, int *err) {
   extern __shared__ __align__(16) char smem[];
-  Tab T;
-  carve_tab(smem, P, T);
-  load_tab(P, T);
-  __syncthreads();
   int lane = threadIdx.x & 31;
+  Tab T;
   W2 w;
-  carve_warp(smem + lay.tab_bytes, P, lay, w);
+  kernel_layout(P, lay, smem, gscratch, 0, T, w);
+  __syncthreads();
   bind_bids(P, gscratch, w);
   if (lane == 0) w.flags[0] = 1;
   for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = map[i];
@@ -1360,16 +1394,14 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns) {
   extern __shared__ __align__(16) char smem[];
-  Tab T;
-  carve_tab(smem, P, T);
-  load_tab(P, T);
-  __syncthreads();
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   int chain = blockIdx.x * wpb + wib;
-  if (chain >= n_chains) return;
+  char *gs = gscratch + (size_t)(chain < n_chains ? chain : 0) * gslice_bytes(P, lay);
+  Tab T;
   W2 w;
-  carve_warp(smem + lay.tab_bytes + wib * lay.warp_bytes, P, lay, w);
-  char *gs = gscratch + (size_t)chain * gscratch_bytes(P.n_slots, P.n_queues);
+  kernel_layout(P, lay, smem, gs, wib, T, w);
+  __syncthreads();
+  if (chain >= n_chains) return;
   bind_bids(P, gs, w);
   if (lane == 0) w.flags[0] = 1;
   __syncwarp();
@@ -1637,6 +1669,11 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   UP(combo_col_off, n_combos + 1);
 #undef UP
   pr->n_combos = n_combos; pr->n_rows = n_rows; pr->n_cols = n_cols;
+  {
+    std::vector<short> l16((size_t)P.n_dev * P.n_dev);
+    for (size_t i = 0; i < l16.size(); ++i) l16[i] = (short)d->link_of[i];
+    if ((rc = upload(ow, l16.data(), l16.size(), &P.link16)) != PS_OK) { ps_problem_destroy(pr); return rc; }
+  }
   // ---- overlap tables: count rows -> scan -> fill, then the column index
   int *cnt = nullptr, *off = nullptr, *ccnt = nullptr, *coff = nullptr;
   void *tmp = nullptr;
@@ -1720,7 +1757,21 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
         if (cw >= target) break;
       }
     }
-    if (bestSC < 0) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "problem too large for shared memory"); }
+    if (getenv("PS_FORCE_GLOBAL_ALL")) bestSC = -1;  // test hook: exercise the global layout
+    if (bestSC < 0) {
+      // nothing fits on chip: block tables and warp slices move to global memory
+      pr->lay.global_all = 1;
+      pr->lay.asg_global = 1;
+      pr->lay.SC = 3 * P.n_slots + 64;
+      pr->lay.GC = P.n_slots + 16;
+      pr->lay.RC = 0;
+      pr->lay.tab_bytes = 0;
+      pr->lay.warp_bytes = al16(warp_bytes_of(P, pr->lay.SC, pr->lay.GC, pr->lay.RC, 1));
+      pr->wpb = 8;
+      pr->smem_per_block = 0;
+      bestW = 8; bestWarps = 8; bestSC = pr->lay.SC;
+    } else {
+      pr->lay.global_all = 0;
     pr->lay.tab_bytes = tb;
     pr->lay.SC = bestSC;
     pr->lay.GC = bestGC;
@@ -1729,6 +1780,7 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
     pr->lay.warp_bytes = al16(warp_bytes_of(P, bestSC, bestGC, bestRC, bestAG));
     pr->wpb = bestW;
     pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
+    }
     pr->blocks_per_sm = std::max(1, bestWarps / bestW);
   }
   // the attribute is per kernel, not per problem: allow the device maximum so
@@ -1825,7 +1877,7 @@ int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t
   if (warps > pr->scratch_warps) {
     cudaFree(pr->scratch);
     size_t want = (size_t)pr->sm_count * pr->blocks_per_sm * wpb;
-    CK(cudaMalloc(&pr->scratch, want * gscratch_bytes(pr->P.n_slots, pr->P.n_queues)));
+    CK(cudaMalloc(&pr->scratch, want * gslice_bytes(pr->P, pr->lay)));
     pr->scratch_warps = want;
   }
   double *dop = nullptr;
@@ -1862,7 +1914,7 @@ int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   unsigned long long *des = nullptr;
   int *cnts = nullptr, *err = nullptr;
   double *dmk = nullptr;
-  CK(cudaMalloc(&scr, gscratch_bytes(pr->P.n_slots, pr->P.n_queues)));
+  CK(cudaMalloc(&scr, gslice_bytes(pr->P, pr->lay)));
   CK(cudaMalloc(&dt, sizeof(ps_trace_task) * (size_t)std::max(task_cap, 1)));
   CK(cudaMalloc(&dep, sizeof(int32_t) * (size_t)std::max(edge_cap, 1)));
   CK(cudaMalloc(&des, sizeof(unsigned long long) * (size_t)std::max(edge_cap, 1)));
@@ -1875,7 +1927,7 @@ int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   TraceSink tr;
   tr.tasks = dt; tr.task_cap = task_cap; tr.n_tasks = cnts; tr.edge_pred = dep; tr.edge_succ = des;
   tr.edge_cap = edge_cap; tr.n_edges = cnts + 1;
-  size_t smem = pr->lay.tab_bytes + pr->lay.warp_bytes;
+  size_t smem = pr->lay.global_all ? 0 : pr->lay.tab_bytes + pr->lay.warp_bytes;
   k_simulate_trace<<<1, 32, smem>>>(pr->P, pr->lay, pr->d_map, pr->d_asg, scr, tr, dmk, err + 2, err);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
@@ -1963,7 +2015,7 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
-  CK(cudaMalloc(&m->scratch, (size_t)n * gscratch_bytes(P.n_slots, P.n_queues)));
+  CK(cudaMalloc(&m->scratch, (size_t)n * gslice_bytes(P, pr->lay)));
   CK(cudaMalloc(&m->d_best, sizeof(double)));
   CK(cudaMalloc(&m->d_bestc, sizeof(int)));
   CK(cudaMemcpy(m->maps, init_map, (size_t)n * P.n_ops * sizeof(int), cudaMemcpyHostToDevice));

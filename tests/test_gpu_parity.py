@@ -281,15 +281,19 @@ def test_exhaustive_optimal_matches_the_reference():
         assert ps.strategy_to_json(res.strategy) == doc["strategy"], doc["name"]
 
 
-def test_in_place_global_assignment_layout(oracle, monkeypatch):
-    """Very wide problems keep device assignments in global memory; force that
-    layout on a small problem and check batch evaluation and MCMC parity."""
-    monkeypatch.setenv("PS_FORCE_ASG_GLOBAL", "1")
+@pytest.mark.parametrize("hook", ["PS_FORCE_ASG_GLOBAL", "PS_FORCE_GLOBAL_ALL"])
+def test_global_memory_layouts(oracle, monkeypatch, hook):
+    """Very wide problems keep device assignments in global memory, and problems
+    too big for shared memory keep every table there; force each layout on a
+    small problem and check batch evaluation, timelines and MCMC parity."""
+    monkeypatch.setenv(hook, "1")
     g, topo, mode, md = _random_case(4242)
     prof = ps.CostProfile()
     strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, s) for s in range(6)]
     got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=md)
     assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies))
+    tg = ps.build_task_graph(g, topo, strategies[1], prof, mode=mode)
+    assert ps.full_simulate(tg).makespan == got[1]
     init = strategies[:3]
     rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=80, seed=7, max_degree=md, mode=mode,
                                                         initial=init, polish=False, rng="philox"))
