@@ -52,6 +52,11 @@ int fail(int code, const std::string &msg) {
   } while (0)
 
 enum { KIND_EDGE = 0, KIND_EDGE_BWD = 1, KIND_OP = 2, KIND_OP_BWD = 3, KIND_SYNC = 4 };
+// ready-set queue field: queue index, plus a flag for tasks known to have no
+// successors (the last hop of a ring), which never bound the lookahead
+#define Q_SINK 0x40000000
+#define Q_MASK 0x3fffffff
+#define INF_BITS 0x7ff0000000000000ull
 
 struct DevProb {
   int n_ops, n_dev, n_kinds, n_links, n_pairs, n_maps, full, n_slots, n_queues, cap;
@@ -290,15 +295,15 @@ __device__ __forceinline__ bool warp_push(bool want, double ready, unsigned long
 //  * Tasks get dense slots per candidate (fbase[o] + k), so the per-task
 //    ready/remaining state of typical strategies also fits in shared memory
 //    (larger candidates fall back to a global scratch slice).
-//  * Conservative lookahead: with LB = min over the ready set of ready+exe,
-//    no task that is not yet ready can become ready before LB (end >= ready +
-//    exe).  Every ready task u with ready_u < LB therefore pops before any
-//    future task, and the heap pops them in (ready, origin) order.  A round
-//    takes, per queue, the minimum-key such task (plus the global minimum),
-//    up to 32 of them on distinct queues, and runs them in parallel: each is
-//    the next task of its queue in the reference's pop order, so start =
-//    max(ready, clock[q]) is exactly the reference's value.
-//    (simulate.py:88-107; proof sketch in DESIGN.md "Lookahead rounds".)
+//  * Conservative lookahead: with LB = min over the ready tasks that have
+//    successors of max(ready, clock[queue]) + exe, no task that is not yet
+//    ready can become ready before LB (its ready time is the end of some
+//    predecessor chain rooted in the ready set, and clocks only grow).  Every
+//    ready task u with ready_u < LB therefore pops before any future task, and
+//    the heap pops them in (ready, origin) order.  A round runs all such tasks
+//    (plus the global minimum): per queue in (ready, origin) order, queues in
+//    parallel, so start = max(ready, clock[q]) is exactly the reference's
+//    value.  (simulate.py:88-107; proof sketch in DESIGN.md "Lookahead rounds".)
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -693,6 +698,7 @@ __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const
   int r = __popcll((long long)msk);
   int da = nth_bit(msk, hop % r), db = nth_bit(msk, (hop + 1) % r);
   if (!link_attrs(P, T, da, db, P.map_shard[w.gmap[a]] / (double)r, q, exe)) { ea = da; eb = db; return false; }
+  if (hop + 1 >= 2 * (r - 1)) q |= Q_SINK;
   return true;
 }
 
@@ -824,14 +830,20 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     unsigned long long mykey = 0;
     double myready = 0.0, myexe = 0.0;
     int myq = -1;
+    int myrank = 0, maxrank = 0;  // position among this round's members on the same queue
     if (n <= 32) {
       // ---- fast path: entry `lane` lives in this lane's registers for the round
       bool valid = lane < n;
       unsigned long long h = valid ? w.rhi[lane] : ~0ull, k = valid ? w.rlo[lane] : ~0ull;
       double e = valid ? w.rexe[lane] : 0.0;
-      int q = valid ? w.rq[lane] : 0;
+      int qr = valid ? w.rq[lane] : 0;
+      int q = qr & Q_MASK;
       double r = __longlong_as_double((long long)h);
-      unsigned long long lbb = valid ? (unsigned long long)__double_as_longlong(r + e) : ~0ull;
+      // LB = min over tasks with successors of max(ready, clock) + exe: no task
+      // outside the ready set can become ready before LB (clocks only grow)
+      double ck = valid ? w.qclock[q] : 0.0;
+      double el = (r < ck ? ck : r) + e;
+      unsigned long long lbb = (valid && !(qr & Q_SINK)) ? (unsigned long long)__double_as_longlong(el) : INF_BITS;
       double LB = __longlong_as_double((long long)warp_min64(lbb, lane));
       bool member = valid && r < LB;
       if (!__any_sync(FULLMASK, member)) {
@@ -839,27 +851,25 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int wl = warp_argmin128(h, k, lane);
         member = lane == wl;
       }
-      // per-queue minimum (ready, origin) among members: each member claims its
-      // queue; a member alone on its queue wins outright, and only queues claimed
-      // twice take a group-restricted lexicographic min
+      // every member runs this round; members sharing a queue run in (ready,
+      // origin) order.  Each member claims its queue; only queues claimed twice
+      // rank their members.
       if (member) w.qown[q & 255] = lane;
       __syncwarp();
       bool lost = member && w.qown[q & 255] != lane;
-      bool win = member;
       if (__any_sync(FULLMASK, lost)) {
-      unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
-      if (member && __popc(gm) > 1) {
-        unsigned cand = gm, v, mn;
-        v = (unsigned)(h >> 32); mn = __reduce_min_sync(gm, v); cand &= __ballot_sync(gm, v == mn);
-        v = (cand >> lane & 1) ? (unsigned)h : 0xffffffffu; mn = __reduce_min_sync(gm, v);
-        cand &= __ballot_sync(gm, v == mn);
-        v = (cand >> lane & 1) ? (unsigned)(k >> 32) : 0xffffffffu; mn = __reduce_min_sync(gm, v);
-        cand &= __ballot_sync(gm, v == mn);
-        v = (cand >> lane & 1) ? (unsigned)k : 0xffffffffu; mn = __reduce_min_sync(gm, v);
-        cand &= __ballot_sync(gm, v == mn);
-        win = (__ffs(cand) - 1) == lane;
+        unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
+        bool multi = member && __popc(gm) > 1;
+        unsigned um = __ballot_sync(FULLMASK, multi);
+        while (um) {
+          int j = __ffs(um) - 1;
+          um &= um - 1;
+          unsigned long long hj = __shfl_sync(FULLMASK, h, j), kj = __shfl_sync(FULLMASK, k, j);
+          if (multi && (gm >> j & 1) && (hj < h || (hj == h && kj < k))) ++myrank;
+        }
+        maxrank = (int)__reduce_max_sync(FULLMASK, (unsigned)myrank);
       }
-      }
+      bool win = member;
       unsigned wb = __ballot_sync(FULLMASK, win);
       nw = __popc(wb);
       if (win && w.flags[0]) { w.qbest[q] = ~0ull; w.qready[q] = ~0ull; }  // bid left by a capped slow round
@@ -867,7 +877,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       unsigned kb = __ballot_sync(FULLMASK, keep);
       if (keep) {
         int pos = __popc(kb & ((1u << lane) - 1u));
-        w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = q;
+        w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = qr;
       }
       n = __popc(kb);
       mine = win;
@@ -876,13 +886,17 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     } else {
       if (lane == 0) w.flags[0] = 1;
       // ---- scan 1: minimum key and LB = min(ready + exe)
-      unsigned long long bh = ~0ull, bl = ~0ull, lb = ~0ull;
+      unsigned long long bh = ~0ull, bl = ~0ull, lb = INF_BITS;
       for (int i = lane; i < n; i += 32) {
         unsigned long long h = w.rhi[i], l = w.rlo[i];
         if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; }
-        double e = __longlong_as_double((long long)h) + w.rexe[i];
-        unsigned long long eb = (unsigned long long)__double_as_longlong(e);
-        if (eb < lb) lb = eb;
+        int qr = w.rq[i];
+        if (!(qr & Q_SINK)) {
+          double r0 = __longlong_as_double((long long)h), ck = w.qclock[qr & Q_MASK];
+          double e = (r0 < ck ? ck : r0) + w.rexe[i];
+          unsigned long long eb = (unsigned long long)__double_as_longlong(e);
+          if (eb < lb) lb = eb;
+        }
       }
       int wl = warp_argmin128(bh, bl, lane);
       unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
@@ -896,7 +910,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         if (i < n) {
           unsigned long long h2 = w.rhi[i];
           mem = __longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey;
-          if (mem) atomicMin(&w.qready[w.rq[i]], h2);
+          if (mem) atomicMin(&w.qready[w.rq[i] & Q_MASK], h2);
         }
         unsigned bm = __ballot_sync(FULLMASK, mem);
         if (mem) w.mem[nm + __popc(bm & ((1u << lane) - 1u))] = i;
@@ -906,7 +920,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // ---- members tied on their queue's ready time bid their origin key
       for (int j = lane; j < nm; j += 32) {
         int i = w.mem[j];
-        int q2 = w.rq[i];
+        int q2 = w.rq[i] & Q_MASK;
         if (w.qready[q2] == w.rhi[i]) atomicMin(&w.qbest[q2], w.rlo[i]);
       }
       __syncwarp();
@@ -918,7 +932,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int i = 0;
         if (j < nm) {
           i = w.mem[j];
-          int q2 = w.rq[i];
+          int q2 = w.rq[i] & Q_MASK;
           win = w.qbest[q2] == w.rlo[i] && w.qready[q2] == w.rhi[i];
         }
         unsigned bm = __ballot_sync(FULLMASK, win);
@@ -934,7 +948,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         mykey = w.rlo[mypos];
         myready = __longlong_as_double((long long)w.rhi[mypos]);
         myexe = w.rexe[mypos];
-        myq = w.rq[mypos];
+        myq = w.rq[mypos] & Q_MASK;
       }
       __syncwarp();
       if (mine0) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rhi[mypos] = ~0ull; }
@@ -963,12 +977,17 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     }
     // ---- run the winners: distinct queues, each its queue's next task
     double end = 0.0, mystart = 0.0;
+    for (int lv = 0; lv <= maxrank; ++lv) {
+      if (mine && myrank == lv) {
+        double clk = w.qclock[myq];
+        double start = myready < clk ? clk : myready;
+        mystart = start;
+        end = start + myexe;
+        w.qclock[myq] = end;
+      }
+      if (maxrank) __syncwarp();
+    }
     if (mine) {
-      double clk = w.qclock[myq];
-      double start = myready < clk ? clk : myready;
-      mystart = start;
-      end = start + myexe;
-      w.qclock[myq] = end;
       if (end > out.makespan) out.makespan = end;
       if (w.opmin && key_kind(mykey) == KIND_OP)
         atomicMin((unsigned long long *)&w.opmin[key_a(mykey)], (unsigned long long)__double_as_longlong(end));
