@@ -28,6 +28,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -74,9 +75,15 @@ struct DevProb {
   const int *row_ent_off, *col_ent_off, *col_ent;
   const unsigned short *ent_k, *ent_l;
   const long long *ent_bytes;
-  const void *ent16, *cent16;  // packed (k | l << 16, bytes) rows and column-ordered copies
+  const void *ent16, *cent16;  // packed Ent32 records: rows, and column-ordered copies
   double mult;                 // backward_multiplier (exe_bwd == exe_fwd * mult, one IEEE product)
-  const short *link16;         // 16-bit copy of link_of (block tables in global mode)
+  const short *link16;         // 16-bit link table: link index, | class << 14 when n_cls > 0
+  // Transfer-time classes: when the links carry at most two distinct (latency,
+  // bandwidth) pairs, every overlap record also holds lat_c + bytes / bw_c for
+  // each class c (the same two IEEE operations), so the simulator reads a
+  // transfer's time instead of dividing.
+  int n_cls;
+  double cls_lat[2], cls_bw[2];
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
@@ -223,16 +230,25 @@ __global__ void k_cols(DevProb P, int n_cols, int n_combos, int *col_count, cons
   if (!col_off_fill) col_count[q] = cnt;
 }
 
-__global__ void k_pack(DevProb P, int n_ent, void *ent16, void *cent16) {
+// 32-byte overlap record: k | l << 16, transfer bytes, and the transfer time
+// on each link class (cost.py:128-130: latency + nbytes / bandwidth)
+struct __align__(16) Ent32 { int kl; int pad; long long bytes; double exe[2]; };
+
+__device__ inline Ent32 make_ent(const DevProb &P, int e) {
+  Ent32 r;
+  r.kl = (int)((unsigned)P.ent_k[e] | ((unsigned)P.ent_l[e] << 16));
+  r.pad = 0;
+  r.bytes = P.ent_bytes[e];
+  for (int c = 0; c < 2; ++c)
+    r.exe[c] = c < P.n_cls ? __dadd_rn(P.cls_lat[c], __ddiv_rn((double)r.bytes, P.cls_bw[c])) : 0.0;
+  return r;
+}
+
+__global__ void k_pack(DevProb P, int n_ent, void *ent32, void *cent32) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_ent) return;
-  long long *dst = (long long *)ent16 + 2 * (size_t)e;
-  dst[0] = (long long)((unsigned)P.ent_k[e] | ((unsigned)P.ent_l[e] << 16));
-  dst[1] = P.ent_bytes[e];
-  int src = P.col_ent[e];
-  long long *cd = (long long *)cent16 + 2 * (size_t)e;
-  cd[0] = (long long)((unsigned)P.ent_k[src] | ((unsigned)P.ent_l[src] << 16));
-  cd[1] = P.ent_bytes[src];
+  ((Ent32 *)ent32)[e] = make_ent(P, e);
+  ((Ent32 *)cent32)[e] = make_ent(P, P.col_ent[e]);
 }
 
 // ---------------------------------------------------------------- simulator
@@ -347,8 +363,8 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
   b += al16(8 * (size_t)P.n_ops) + 16 + 128;         // per-op forward exe cache, flags, winner lanes
-  b += 4 * 256;                                      // queue claims (hashed)
-  b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC);  // counters: ready, remaining, shard id
+  b += 256;                                          // queue claims (hashed, claiming lane)
+  b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC / 2);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
   b += 256 + 128 + 16;                               // proposal staging, phase counters
@@ -365,7 +381,7 @@ struct W2 {
   double *exef;
   int *flags;  // [0]: slow-path queue bids may be dirty
   int *wlane;  // [32] lane holding the k-th winner of the round
-  int *qown;   // [Q] last member to claim the queue this round
+  unsigned char *qown;  // [256] last member to claim the (hashed) queue this round
   int rcap;    // ready-set capacity in effect (shared memory, or the global overflow slice)
   double *opmin;  // optional [n_ops]: earliest end of each op's forward tasks (exhaustive bounds)
   const TraceSink *tr;  // optional: record every task and dependency (API materialisation)
@@ -429,7 +445,7 @@ __device__ inline void load_tab(const DevProb &P, const Tab &t) {
   for (int i = tid; i <= P.n_pairs; i += nt) t.combo_off[i] = P.combo_off[i];
   for (int i = tid; i < P.n_ops; i += nt) t.op_param_mask[i] = P.op_param_mask[i];
   for (int i = tid; i < P.n_dev; i += nt) t.dev_kind[i] = P.dev_kind[i];
-  for (int i = tid; i < P.n_dev * P.n_dev; i += nt) t.link_of[i] = (short)P.link_of[i];
+  for (int i = tid; i < P.n_dev * P.n_dev; i += nt) t.link_of[i] = P.link16[i];
 }
 
 __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2 &w) {
@@ -451,10 +467,10 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.exef = (double *)take(8 * P.n_ops);
   w.flags = (int *)take(16);
   w.wlane = (int *)take(128);
-  w.qown = (int *)take(4 * 256);
+  w.qown = (unsigned char *)take(256);
   w.cready = (double *)take(8 * L.SC);
   w.crem = (unsigned short *)take(2 * L.SC);
-  w.cgrp = (unsigned char *)take(L.SC);
+  w.cgrp = (unsigned char *)take(L.SC / 2);  // forward slots only: 2 Tf + G <= SC
   w.gmask = (unsigned long long *)take(8 * L.GC);
   w.srow = (int *)take(4 * L.RC);
   w.scol = (int *)take(4 * L.RC);
@@ -528,8 +544,15 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 // the ready set in global memory (same answer, slower).
 __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch,
                                       int lane) {
-  SimOut o = warp_simulate2(P, T, w, L, gscratch, lane);
-  if (o.status == PS_STATUS_CAPACITY) o = warp_simulate2(P, T, with_global_ready_set(P, gscratch, w), L, gscratch, lane);
+  // one inlined copy of the simulator per call site (the code is large: keep it in the instruction cache)
+  SimOut o;
+  W2 wg = w;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    o = warp_simulate2(P, T, wg, L, gscratch, lane);
+    if (o.status != PS_STATUS_CAPACITY) break;
+    wg = with_global_ready_set(P, gscratch, w);
+  }
   return o;
 }
 
@@ -677,8 +700,9 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
 // exe time / queue of a transfer between devices da -> db carrying nb bytes
 __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int da, int db, double nb, int &q,
                                            double &exe) {
-  int li = T.link_of[da * P.n_dev + db];
-  if (li < 0) return false;
+  int lv = T.link_of[da * P.n_dev + db];
+  if (lv < 0) return false;
+  int li = P.n_cls ? (lv & 0x3fff) : lv;
   q = P.n_dev + li;
   exe = __ldg(&T.link_lat[li]) + nb / __ldg(&T.link_bw[li]);
   return true;
@@ -702,7 +726,16 @@ __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const
   return true;
 }
 
-struct Ent16 { int kl; int pad; long long bytes; };  // k | l << 16, transfer bytes
+// queue / time of the transfer an overlap record creates between da -> db
+__device__ __forceinline__ bool link_attrs_ent(const DevProb &P, const Tab &T, int da, int db, const Ent32 &en,
+                                               int &q, double &exe) {
+  if (!P.n_cls) return link_attrs(P, T, da, db, (double)en.bytes, q, exe);
+  int lv = T.link_of[da * P.n_dev + db];
+  if (lv < 0) return false;
+  q = P.n_dev + (lv & 0x3fff);
+  exe = (lv >> 14) ? en.exe[1] : en.exe[0];
+  return true;
+}
 
 #ifdef PS_PHASES
 __device__ unsigned long long g_phase[16];
@@ -748,8 +781,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   PH_CNT(9, st.rowoff == w.srow ? 1 : 0);
   const int Tf = st.Tf;
   PH_CNT(10, (P.full ? 2 * Tf + st.G : Tf) <= L.SC ? 1 : 0);
-  const Ent16 *ent = (const Ent16 *)P.ent16;
-  const Ent16 *cent = (const Ent16 *)P.cent16;
+  const Ent32 *ent = (const Ent32 *)P.ent16;
+  const Ent32 *cent = (const Ent32 *)P.cent16;
   const bool was_dirty = w.flags[0] != 0;
   for (int q = lane; q < P.n_queues; q += 32) {
     w.qclock[q] = 0.0;
@@ -845,6 +878,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       double el = (r < ck ? ck : r) + e;
       unsigned long long lbb = (valid && !(qr & Q_SINK)) ? (unsigned long long)__double_as_longlong(el) : INF_BITS;
       double LB = __longlong_as_double((long long)warp_min64(lbb, lane));
+      PH_ADD(5, t_sel);
+      PH_T(t_cl);
       bool member = valid && r < LB;
       if (!__any_sync(FULLMASK, member)) {
         // degenerate (zero or absorbed exe): the global minimum alone
@@ -883,6 +918,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       mine = win;
       if (win) w.wlane[__popc(wb & ((1u << lane) - 1u))] = lane;
       mykey = k; myready = r; myexe = e; myq = q;
+      PH_ADD(15, t_cl);
     } else {
       if (lane == 0) w.flags[0] = 1;
       // ---- scan 1: minimum key and LB = min(ready + exe)
@@ -1020,8 +1056,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
     int wdev = 0, head = 0, tail = 0, L = 0, ring = 0;
     int fe = -1, fp = 0;  // this lane's first list entry (index j0) and its pair
-    Ent16 fen;
-    fen.kl = 0; fen.pad = 0; fen.bytes = 0;
+    Ent32 fen;
+    fen.kl = 0; fen.pad = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
     if (act_lane) {
       if (kind == KIND_OP || kind == KIND_OP_BWD) wdev = w.asg[T.op_slot_off[a] + c];
       if (kind == KIND_OP) {
@@ -1079,7 +1115,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           if (idx < head) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
           else {
             int r = idx - head;
-            Ent16 en = fen;
+            Ent32 en = fen;
             int p = fp;
             if (t > 0) {
               for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
@@ -1099,7 +1135,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
                 else {
                   act = 2;
                   skey = pack_key(KIND_EDGE, a, dp, c, l);
-                  if (!link_attrs(P, T, wdev, ddev, (double)en.bytes, pq, pexe)) { err = true; ea = wdev; eb = ddev; }
+                  if (!link_attrs_ent(P, T, wdev, ddev, en, pq, pexe)) { err = true; ea = wdev; eb = ddev; }
                 }
               }
             }
@@ -1108,7 +1144,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           if (idx >= L - tail) { act = 1; slot = 2 * Tf + w.gbase[a] + ring; skey = pack_key(KIND_SYNC, a, ring, 0, 0); }
           else {
             int r = idx;
-            Ent16 en = fen;
+            Ent32 en = fen;
             int p = fp;
             if (t > 0) {
               for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
@@ -1128,7 +1164,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
                 else {
                   act = 2;
                   skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c);
-                  if (!link_attrs(P, T, sdev, wdev, (double)en.bytes, pq, pexe)) { err = true; ea = sdev; eb = wdev; }
+                  if (!link_attrs_ent(P, T, sdev, wdev, en, pq, pexe)) { err = true; ea = sdev; eb = wdev; }
                 }
               }
             }
@@ -1444,20 +1480,6 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   if (rng_mode == PS_RNG_PHILOX && rng.bpos < 4) philox_block(rng.ctr - 1, rng.key, rng.buf);
   int *bmap = best_maps + (size_t)chain * P.n_ops;
   unsigned char *basg = best_asgs + (size_t)chain * P.n_slots;
-  if (!cs.started) {
-    SimOut o = simulate_any(P, T, w, lay, gs, lane);
-    cs.started = 1;
-    if (o.status != PS_STATUS_OK) {
-      cs.status = o.status; cs.err_a = o.err_a; cs.err_b = o.err_b;
-      cs.initial = cs.best = cs.cost = __longlong_as_double(0x7ff0000000000000ll);
-      if (lane == 0) st[chain] = cs;
-      return;
-    }
-    cs.cost = cs.best = cs.initial = o.makespan;
-    cs.beta = beta_given ? beta_param : (o.makespan > 0.0 ? __ddiv_rn(ln10, __dmul_rn(0.05, o.makespan)) : 1.0);
-    for (int i = lane; i < P.n_ops; i += 32) bmap[i] = w.mapl[i];
-    for (int i = lane; i < P.n_slots; i += 32) basg[i] = w.asg[i];
-  }
   unsigned long long t0 = globaltimer_ns();
 #ifdef PS_PHASES
   for (int i = lane; i < 16; i += 32) w.ph[i] = 0;
@@ -1465,32 +1487,38 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
 #endif
   PH_T(t_loop);
   int n_it = 0;
-  for (int it = 0; it < proposals; ++it) {
-    ++n_it;
-    if (budget_ns) {  // time-boxed segment: stop between proposals once the budget is spent
-      unsigned long long now = __shfl_sync(FULLMASK, globaltimer_ns(), 0);
-      if (now - t0 >= budget_ns) break;
-    }
-    // _propose_change (search.py:101-115): op, degree map, one device per task
-    int o = (int)rng.below((unsigned)P.n_ops);
-    int m = (int)rng.below((unsigned)P.op_nmaps_enum[o]);
-    cs.last_op = o;
-    int g = T.op_map_off[o] + m;
-    int size = P.map_size[g];
-    int base = T.op_slot_off[o];
-    int old_m = w.mapl[o];
-    int old_size = P.map_size[T.op_map_off[o] + old_m];
-    bool same = (m == old_m);
-    for (int i = lane; i < old_size; i += 32) w.oldasg[i] = w.asg[base + i];
-    __syncwarp();
-    for (int k = 0; k < size; ++k) {
-      unsigned dv = rng.below((unsigned)P.n_dev);
-      same = same && (k < old_size && w.oldasg[k] == (unsigned char)dv);
+  // iteration -1 scores the chain's initial strategy (first launch only); the
+  // simulator has a single call site so the kernel holds one copy of it
+  for (int it = cs.started ? 0 : -1; it < proposals; ++it) {
+    int o = 0, m = 0, base = 0, old_m = 0, old_size = 0;
+    bool same = false;
+    if (it >= 0) {
+      ++n_it;
+      if (budget_ns) {  // time-boxed segment: stop between proposals once the budget is spent
+        unsigned long long now = __shfl_sync(FULLMASK, globaltimer_ns(), 0);
+        if (now - t0 >= budget_ns) break;
+      }
+      // _propose_change (search.py:101-115): op, degree map, one device per task
+      o = (int)rng.below((unsigned)P.n_ops);
+      m = (int)rng.below((unsigned)P.op_nmaps_enum[o]);
+      cs.last_op = o;
+      int g = T.op_map_off[o] + m;
+      int size = P.map_size[g];
+      base = T.op_slot_off[o];
+      old_m = w.mapl[o];
+      old_size = P.map_size[T.op_map_off[o] + old_m];
+      same = (m == old_m);
+      for (int i = lane; i < old_size; i += 32) w.oldasg[i] = w.asg[base + i];
       __syncwarp();
-      if (lane == 0) w.asg[base + k] = (unsigned char)dv;
+      for (int k = 0; k < size; ++k) {
+        unsigned dv = rng.below((unsigned)P.n_dev);
+        same = same && (k < old_size && w.oldasg[k] == (unsigned char)dv);
+        __syncwarp();
+        if (lane == 0) w.asg[base + k] = (unsigned char)dv;
+      }
+      if (lane == 0) w.mapl[o] = m;
+      __syncwarp();
     }
-    if (lane == 0) w.mapl[o] = m;
-    __syncwarp();
     double cand;
     if (same) {
       cand = cs.cost;
@@ -1498,9 +1526,25 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
       SimOut so = simulate_any(P, T, w, lay, gs, lane);
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
+        if (it < 0) {
+          cs.started = 1;
+          cs.initial = cs.best = cs.cost = __longlong_as_double(0x7ff0000000000000ll);
+          if (lane == 0) st[chain] = cs;
+          return;
+        }
         break;
       }
       cand = so.makespan;
+    }
+    if (it < 0) {
+      cs.started = 1;
+      cs.cost = cs.best = cs.initial = cand;
+      cs.beta = beta_given ? beta_param : (cand > 0.0 ? __ddiv_rn(ln10, __dmul_rn(0.05, cand)) : 1.0);
+      for (int i = lane; i < P.n_ops; i += 32) bmap[i] = w.mapl[i];
+      for (int i = lane; i < P.n_slots; i += 32) basg[i] = w.asg[i];
+      __syncwarp();
+      t0 = globaltimer_ns();
+      continue;
     }
     long long idx = cs.proposals++;
     bool ok;
@@ -1689,8 +1733,25 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
 #undef UP
   pr->n_combos = n_combos; pr->n_rows = n_rows; pr->n_cols = n_cols;
   {
+    // link classes: distinct (latency, bandwidth) bit patterns, if at most two
+    std::vector<int> cls(P.n_links, 0);
+    int ncls = 0;
+    for (int li = 0; li < P.n_links && ncls <= 2; ++li) {
+      int c = 0;
+      while (c < ncls && !(memcmp(&P.cls_lat[c], &d->link_lat[li], 8) == 0 &&
+                           memcmp(&P.cls_bw[c], &d->link_bw[li], 8) == 0)) ++c;
+      if (c == ncls) {
+        if (ncls == 2) { ncls = 3; break; }
+        P.cls_lat[c] = d->link_lat[li]; P.cls_bw[c] = d->link_bw[li]; ++ncls;
+      }
+      cls[li] = c;
+    }
+    P.n_cls = (ncls <= 2 && P.n_links < 16384) ? ncls : 0;
     std::vector<short> l16((size_t)P.n_dev * P.n_dev);
-    for (size_t i = 0; i < l16.size(); ++i) l16[i] = (short)d->link_of[i];
+    for (size_t i = 0; i < l16.size(); ++i) {
+      int li = d->link_of[i];
+      l16[i] = (short)(li < 0 ? -1 : (P.n_cls ? (li | cls[li] << 14) : li));
+    }
     if ((rc = upload(ow, l16.data(), l16.size(), &P.link16)) != PS_OK) { ps_problem_destroy(pr); return rc; }
   }
   // ---- overlap tables: count rows -> scan -> fill, then the column index
@@ -1732,8 +1793,8 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   if (n_cols) k_cols<<<(n_cols + 127) / 128, 128>>>(P, n_cols, n_combos, nullptr, coff);
   CK(cudaGetLastError());
   void *e16 = nullptr, *c16 = nullptr;
-  CK(cudaMalloc(&e16, (size_t)(n_ent + 1) * 16));
-  CK(cudaMalloc(&c16, (size_t)(n_ent + 1) * 16));
+  CK(cudaMalloc(&e16, (size_t)(n_ent + 1) * sizeof(Ent32)));
+  CK(cudaMalloc(&c16, (size_t)(n_ent + 1) * sizeof(Ent32)));
   ow.push_back(e16); ow.push_back(c16);
   P.ent16 = e16; P.cent16 = c16;
   if (n_ent) k_pack<<<(n_ent + 127) / 128, 128>>>(P, n_ent, e16, c16);
@@ -1754,13 +1815,17 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
     int target = 7;  // 7 x 148 SMs = 1036 resident chains >= the 1024-chain workload
     if (const char *e = getenv("PS_TARGET_WARPS_PER_SM")) target = std::max(1, atoi(e));
     int bestSC = -1, bestW = 0, bestWarps = 0, bestRC = 0, bestGC = 0, bestAG = 0;
-    const int caps[] = {4096, 3072, 2048, 1536, 1280, 1024, 896, 768, 640, 512, 384, 256, 128, 0};
+    std::vector<int> caps;
+    for (int c = 4096; c >= 128; c -= 32) caps.push_back(c);
+    caps.push_back(0);
     int ag0 = getenv("PS_FORCE_ASG_GLOBAL") ? 1 : 0;  // test hook: exercise the in-place path
     for (int ag = ag0; ag < 2 && bestWarps < target; ++ag) {
-      for (int ci = 0; ci < (int)(sizeof caps / sizeof caps[0]); ++ci) {
+      for (int ci = 0; ci < (int)caps.size(); ++ci) {
+        // ring shards and staged rows / columns sized in proportion to the task
+        // counters (typical full-iteration candidates: G ~ 0.19, rows ~ 0.69 of 2 Tf + G)
         int SC = caps[ci];
-        int GC = std::max(16, SC / 4);
-        int RC = std::max(64, 3 * SC / 4);
+        int GC = std::max(16, (SC * 5 + 23) / 24);
+        int RC = std::max(64, SC * 11 / 16);
         size_t wb = al16(warp_bytes_of(P, SC, GC, RC, ag));
         int cw = 0, cwp = 0;
         for (int wp : {8, 7, 6, 5, 4, 3, 2, 1}) {

@@ -27,7 +27,7 @@ nat.check(L.ps_debug_phases(nat.ptr(ph), 1), "phases")
 nat.check(L.ps_mcmc_run_budget(h, 1 << 30, 100_000_000, None), "run")
 nat.check(L.ps_debug_phases(nat.ptr(ph), 1), "phases")
 info = low.info()
-names = ["setup", "init", "select", "succ-setup", "succ-iters", "-", "mcmc-loop", "proposals", "sims", "rows-staged",
+names = ["setup", "init", "select", "succ-setup", "succ-iters", "sel:LB(fast)", "mcmc-loop", "proposals", "sims", "rows-staged",
          "state-in-smem", "rounds", "sum-n", "winners", "iters"]
 sims = ph[8]; rounds = ph[11]
 print(f"mode={mode} chains={C} SC={info.shared_counters} warps/SM={info.resident_warps_per_sm} wpb={info.warps_per_block}")
@@ -35,7 +35,8 @@ print(f"sims={sims} proposals={ph[7]} rounds/sim={rounds/max(sims,1):.1f} avg n=
       f"winners/round={ph[13]/max(rounds,1):.2f} iters/round={ph[14]/max(rounds,1):.2f} rows staged={ph[9]/max(sims,1):.2f} "
       f"state in smem={ph[10]/max(sims,1):.2f}")
 tot = ph[6]
-for i in (0, 1, 2, 3, 4):
+names.append("sel:claim+compact(fast)")
+for i in (0, 1, 2, 5, 15, 3, 4):
     print(f"{names[i]:12s} {ph[i]/max(sims,1):12.0f} cycles/sim  {100*ph[i]/max(tot,1):5.1f}% of loop   "
           f"{ph[i]/max(rounds,1):8.0f} cycles/round")
 print(f"loop total {tot/max(sims,1):.0f} cycles/sim")
