@@ -1042,7 +1042,13 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     PH_ADD(2, t_sel);
     PH_CNT(13, nw);
     PH_T(t_succ);
-    // ---- successors: lane groups of G per winner, random access into each list
+    // ---- successors: lane groups of G per winner, random access into each list.
+    // A winner's successors are its overlap-list entries (forward op: row c of
+    // each out-pair's current combo; backward op: column c of each in-pair's)
+    // plus at most one fixed successor, taken last: forward -> its backward
+    // task, backward -> its ring's hop 0, transfer -> the task it feeds, ring
+    // hop -> the next hop.  Entries of both directions go through one code path
+    // (taskgraph.py:199-221: same device -> dependency, else a transfer).
     int lg = 31 - __clz(nw);
     if ((1 << lg) < nw) ++lg;
     int G = 32 >> lg, lgG = 5 - lg;
@@ -1054,49 +1060,56 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     double wend = __shfl_sync(FULLMASK, end, srcl);
     int wrec = __shfl_sync(FULLMASK, myrec, srcl);
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
-    int wdev = 0, head = 0, tail = 0, L = 0, ring = 0;
+    const bool fwd = kind == KIND_OP;
+    const int *poff = fwd ? T.op_out_off : T.op_in_off;
+    const int *plist = fwd ? T.op_out_pairs : T.op_in_pairs;
+    const int *pbase = fwd ? w.prow : w.pcol;
+    const int *eoff = fwd ? st.rowoff : st.coloff;
+    const Ent32 *etab = fwd ? ent : cent;
+    int wdev = 0, L = 0;
     int fe = -1, fp = 0;  // this lane's first list entry (index j0) and its pair
-    Ent32 fen;
-    fen.kl = 0; fen.pad = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
+    // fixed successor: fact 1 = arrive at counter fslot, 2 = push task fkey directly
+    int fact = 0, fslot = 0, fq = 0, fea = -1, feb = -1;
+    unsigned long long fkey = 0;
+    double fexe = 0.0;
+    bool ferr = false;
     if (act_lane) {
-      if (kind == KIND_OP || kind == KIND_OP_BWD) wdev = w.asg[T.op_slot_off[a] + c];
-      if (kind == KIND_OP) {
-        head = P.full ? 1 : 0;
-        L = head;
-        int r0 = j0 - head;
-        for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
-          int p = T.op_out_pairs[i];
-          int row = w.prow[p] + c;
-          int e0 = st.rowoff[row], len = st.rowoff[row + 1] - e0;
+      if (fwd || kind == KIND_OP_BWD) {
+        wdev = w.asg[T.op_slot_off[a] + c];
+        int r0 = j0;
+        for (int i = poff[a]; i < poff[a + 1]; ++i) {
+          int p = plist[i];
+          int ix = pbase[p] + c;
+          int e0 = eoff[ix], len = eoff[ix + 1] - e0;
           if (fe < 0 && r0 >= 0 && r0 < len) { fe = e0 + r0; fp = p; }
           r0 -= len;
           L += len;
         }
-        if (fe >= 0) fen = ent[fe];
-      } else if (kind == KIND_OP_BWD) {
-        int r0 = j0;
-        for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
-          int p = T.op_in_pairs[i];
-          int col = w.pcol[p] + c;
-          int j1 = st.coloff[col], len = st.coloff[col + 1] - j1;
-          if (fe < 0 && r0 >= 0 && r0 < len) { fe = j1 + r0; fp = p; }
-          r0 -= len;
-          L += len;
-        }
-        if (fe >= 0) fen = cent[fe];
-        if (T.op_param_mask[a] >= 0) {
+        if (fwd) {
+          if (P.full) { fact = 1; fslot = Tf + w.fbase[a] + c; fkey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
+        } else if (T.op_param_mask[a] >= 0) {
           int si = st.grp[w.fbase[a] + c];
-          if (__popcll((long long)st.gmask[w.gbase[a] + si]) >= 2) { tail = 1; ring = si; }
+          if (__popcll((long long)st.gmask[w.gbase[a] + si]) >= 2) {
+            fact = 1; fslot = 2 * Tf + w.gbase[a] + si; fkey = pack_key(KIND_SYNC, a, si, 0, 0);
+          }
         }
-        L += tail;
-      } else if (kind == KIND_SYNC) {
+      } else if (kind == KIND_EDGE) {
+        fact = 1; fslot = w.fbase[b] + d; fkey = pack_key(KIND_OP, b, 0, d, 0);
+      } else if (kind == KIND_EDGE_BWD) {
+        fact = 1; fslot = Tf + w.fbase[a] + c; fkey = pack_key(KIND_OP_BWD, a, 0, c, 0);
+      } else {  // ring hop c -> c + 1 (none after the last)
         int r = __popcll((long long)st.gmask[w.gbase[a] + b]);
-        L = ((int)c + 1 < 2 * (r - 1)) ? 1 : 0;
-      } else {
-        L = 1;
+        if ((int)c + 1 < 2 * (r - 1)) {
+          fact = 2; fkey = pack_key(KIND_SYNC, a, b, c + 1, 0);
+          if (!sync_attrs(P, T, w, st, a, b, c + 1, fq, fexe, fea, feb)) ferr = true;
+        }
       }
     }
-    int iters = (L + G - 1) >> lgG;
+    Ent32 fen;
+    fen.kl = 0; fen.pad = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
+    if (fe >= 0) fen = etab[fe];
+    int Lt = L + (fact ? 1 : 0);
+    int iters = (Lt + G - 1) >> lgG;
     iters = (int)__reduce_max_sync(FULLMASK, (unsigned)(act_lane ? iters : 0));
     PH_ADD(3, t_succ);
     PH_CNT(14, iters);
@@ -1111,71 +1124,37 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       bool err = false;
       int ea = -1, eb = -1;
       if (act_lane && idx < L) {
-        if (kind == KIND_OP) {
-          if (idx < head) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
-          else {
-            int r = idx - head;
-            Ent32 en = fen;
-            int p = fp;
-            if (t > 0) {
-              for (int i = T.op_out_off[a]; i < T.op_out_off[a + 1]; ++i) {
-                p = T.op_out_pairs[i];
-                int row = w.prow[p] + c;
-                int e0 = st.rowoff[row], len = st.rowoff[row + 1] - e0;
-                if (r < len) { en = ent[e0 + r]; break; }
-                r -= len;
-              }
-            }
-            {
-              {
-                int dp = T.pair_dst[p];
-                int l = en.kl >> 16;
-                int ddev = w.asg[T.op_slot_off[dp] + l];
-                if (ddev == wdev) { act = 1; slot = w.fbase[dp] + l; skey = pack_key(KIND_OP, dp, 0, l, 0); }
-                else {
-                  act = 2;
-                  skey = pack_key(KIND_EDGE, a, dp, c, l);
-                  if (!link_attrs_ent(P, T, wdev, ddev, en, pq, pexe)) { err = true; ea = wdev; eb = ddev; }
-                }
-              }
-            }
+        Ent32 en = fen;
+        int p = fp;
+        if (t > 0) {
+          int r = idx;
+          for (int i = poff[a]; i < poff[a + 1]; ++i) {
+            p = plist[i];
+            int ix = pbase[p] + c;
+            int e0 = eoff[ix], len = eoff[ix + 1] - e0;
+            if (r < len) { en = etab[e0 + r]; break; }
+            r -= len;
           }
-        } else if (kind == KIND_OP_BWD) {
-          if (idx >= L - tail) { act = 1; slot = 2 * Tf + w.gbase[a] + ring; skey = pack_key(KIND_SYNC, a, ring, 0, 0); }
-          else {
-            int r = idx;
-            Ent32 en = fen;
-            int p = fp;
-            if (t > 0) {
-              for (int i = T.op_in_off[a]; i < T.op_in_off[a + 1]; ++i) {
-                p = T.op_in_pairs[i];
-                int col = w.pcol[p] + c;
-                int j1 = st.coloff[col], len = st.coloff[col + 1] - j1;
-                if (r < len) { en = cent[j1 + r]; break; }
-                r -= len;
-              }
-            }
-            {
-              {
-                int sp = T.pair_src[p];
-                int kk = en.kl & 0xffff;
-                int sdev = w.asg[T.op_slot_off[sp] + kk];
-                if (sdev == wdev) { act = 1; slot = Tf + w.fbase[sp] + kk; skey = pack_key(KIND_OP_BWD, sp, 0, kk, 0); }
-                else {
-                  act = 2;
-                  skey = pack_key(KIND_EDGE_BWD, sp, a, kk, c);
-                  if (!link_attrs_ent(P, T, sdev, wdev, en, pq, pexe)) { err = true; ea = sdev; eb = wdev; }
-                }
-              }
-            }
-          }
-        } else if (kind == KIND_EDGE) { act = 1; slot = w.fbase[b] + d; skey = pack_key(KIND_OP, b, 0, d, 0); }
-        else if (kind == KIND_EDGE_BWD) { act = 1; slot = Tf + w.fbase[a] + c; skey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
-        else {
-          act = 2;
-          skey = pack_key(KIND_SYNC, a, b, c + 1, 0);
-          if (!sync_attrs(P, T, w, st, a, b, c + 1, pq, pexe, ea, eb)) err = true;
         }
+        // the entry's other end: forward -> consumer block l, backward -> producer block k
+        int kk = en.kl & 0xffff, l = en.kl >> 16;
+        int xo = fwd ? T.pair_dst[p] : T.pair_src[p];
+        int xb = fwd ? l : kk;
+        int xdev = w.asg[T.op_slot_off[xo] + xb];
+        if (xdev == wdev) {
+          act = 1;
+          slot = (fwd ? 0 : Tf) + w.fbase[xo] + xb;
+          skey = pack_key(fwd ? KIND_OP : KIND_OP_BWD, xo, 0, xb, 0);
+        } else {
+          // transfer (producer op, consumer op, producer block, consumer block)
+          act = 2;
+          int so = fwd ? (int)a : xo, dop = fwd ? xo : (int)a, sb = fwd ? (int)c : kk, db = fwd ? l : (int)c;
+          int sdv = fwd ? wdev : xdev, ddv = fwd ? xdev : wdev;
+          skey = pack_key(fwd ? KIND_EDGE : KIND_EDGE_BWD, so, dop, sb, db);
+          if (!link_attrs_ent(P, T, sdv, ddv, en, pq, pexe)) { err = true; ea = sdv; eb = ddv; }
+        }
+      } else if (act_lane && idx == L && fact) {
+        act = fact; slot = fslot; skey = fkey; pq = fq; pexe = fexe; err = ferr; ea = fea; eb = feb;
       }
       if (w.tr && act != 0 && wrec >= 0) {
         int e_ = atomicAdd(w.tr->n_edges, 1);
