@@ -280,7 +280,7 @@ struct SimOut {
 
 
 __device__ __forceinline__ int nth_bit(unsigned long long m, int n) {
-  for (int i = 0; i < n; ++i) m &= m - 1;
+  for (int i = 0; i < n; ++i) m &= m - 1;  // (__fns is a long software sequence)
   return __ffsll((long long)m) - 1;
 }
 
@@ -363,7 +363,6 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
   b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
   b += al16(8 * (size_t)P.n_ops) + 16 + 128;         // per-op forward exe cache, flags, winner lanes
-  b += 256;                                          // queue claims (hashed, claiming lane)
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC / 2);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
@@ -381,7 +380,6 @@ struct W2 {
   double *exef;
   int *flags;  // [0]: slow-path queue bids may be dirty
   int *wlane;  // [32] lane holding the k-th winner of the round
-  unsigned char *qown;  // [256] last member to claim the (hashed) queue this round
   int rcap;    // ready-set capacity in effect (shared memory, or the global overflow slice)
   double *opmin;  // optional [n_ops]: earliest end of each op's forward tasks (exhaustive bounds)
   const TraceSink *tr;  // optional: record every task and dependency (API materialisation)
@@ -467,7 +465,6 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.exef = (double *)take(8 * P.n_ops);
   w.flags = (int *)take(16);
   w.wlane = (int *)take(128);
-  w.qown = (unsigned char *)take(256);
   w.cready = (double *)take(8 * L.SC);
   w.crem = (unsigned short *)take(2 * L.SC);
   w.cgrp = (unsigned char *)take(L.SC / 2);  // forward slots only: 2 Tf + G <= SC
@@ -702,9 +699,13 @@ __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int d
                                            double &exe) {
   int lv = T.link_of[da * P.n_dev + db];
   if (lv < 0) return false;
-  int li = P.n_cls ? (lv & 0x3fff) : lv;
-  q = P.n_dev + li;
-  exe = __ldg(&T.link_lat[li]) + nb / __ldg(&T.link_bw[li]);
+  if (P.n_cls) {
+    q = P.n_dev + (lv & 0x3fff);
+    exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + nb / ((lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
+  } else {
+    q = P.n_dev + lv;
+    exe = __ldg(&T.link_lat[lv]) + nb / __ldg(&T.link_bw[lv]);
+  }
   return true;
 }
 
@@ -718,10 +719,18 @@ __device__ __forceinline__ void op_attrs(const DevProb &P, const Tab &T, const W
 
 __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const W2 &w, const State &st, int a, int si,
                                            int hop, int &q, double &exe, int &ea, int &eb) {
-  unsigned long long msk = st.gmask[w.gbase[a] + si];
+  int gi = w.gbase[a] + si;
+  unsigned long long msk = st.gmask[gi];
   int r = __popcll((long long)msk);
-  int da = nth_bit(msk, hop % r), db = nth_bit(msk, (hop + 1) % r);
-  if (!link_attrs(P, T, da, db, P.map_shard[w.gmap[a]] / (double)r, q, exe)) { ea = da; eb = db; return false; }
+  int h0 = hop < r ? hop : hop - r, h1 = hop + 1 < r ? hop + 1 : hop + 1 - r;  // hop < 2 (r - 1)
+  int da = nth_bit(msk, h0), db = nth_bit(msk, h1);
+  // bytes per hop (taskgraph.py:245): computed when hop 0 becomes ready and
+  // kept in the ring's counter slot, which is free from then on
+  double *per = &st.ready[2 * st.Tf + gi];
+  double nb;
+  if (hop == 0) { nb = P.map_shard[w.gmap[a]] / (double)r; *per = nb; }
+  else nb = *per;
+  if (!link_attrs(P, T, da, db, nb, q, exe)) { ea = da; eb = db; return false; }
   if (hop + 1 >= 2 * (r - 1)) q |= Q_SINK;
   return true;
 }
@@ -737,6 +746,14 @@ __device__ __forceinline__ bool link_attrs_ent(const DevProb &P, const Tab &T, i
   return true;
 }
 
+#ifdef PS_TCYC
+// cycle timeline of one simulation of warp 0 of block 0 (debug builds)
+__device__ long long g_tc[4096 * 16];
+__device__ int g_tc_sim;
+#define TC(i) do { if (tc_on && lane == 0 && tc_r < 4096) g_tc[tc_r * 16 + (i)] = clock64(); } while (0)
+#else
+#define TC(i)
+#endif
 #ifdef PS_PHASES
 __device__ unsigned long long g_phase[16];
 #define PH_T(v) long long v = clock64()
@@ -774,6 +791,11 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   out.makespan = 0.0;
   out.status = PS_STATUS_OK;
   out.err_a = out.err_b = -1;
+#ifdef PS_TCYC
+  bool tc_on = false;
+  int tc_r = 0;
+  if (threadIdx.x == 0 && blockIdx.x == 1) tc_on = atomicAdd(&g_tc_sim, 1) == 5;
+#endif
   PH_T(t_setup);
   State st = setup_candidate(P, T, w, L, gscratch, lane);
   PH_ADD(0, t_setup);
@@ -790,6 +812,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   }
   __syncwarp();
   if (lane == 0) w.flags[0] = 0;
+  bool dirty = false;  // register copy of w.flags[0] for this simulation
   if (P.full)
     for (int s = lane; s < st.G; s += 32) st.gmask[s] = 0ull;
   __syncwarp();
@@ -856,6 +879,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
   while (n > 0) {
     PH_T(t_sel);
+    TC(0);
     PH_CNT(11, 1);
     PH_CNT(12, n);
     bool mine = false;
@@ -876,9 +900,11 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // outside the ready set can become ready before LB (clocks only grow)
       double ck = valid ? w.qclock[q] : 0.0;
       double el = (r < ck ? ck : r) + e;
+      TC(1);
       unsigned long long lbb = (valid && !(qr & Q_SINK)) ? (unsigned long long)__double_as_longlong(el) : INF_BITS;
       double LB = __longlong_as_double((long long)warp_min64(lbb, lane));
       PH_ADD(5, t_sel);
+      TC(2);
       PH_T(t_cl);
       bool member = valid && r < LB;
       if (!__any_sync(FULLMASK, member)) {
@@ -887,27 +913,29 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         member = lane == wl;
       }
       // every member runs this round; members sharing a queue run in (ready,
-      // origin) order.  Each member claims its queue; only queues claimed twice
-      // rank their members.
-      if (member) w.qown[q & 255] = lane;
-      __syncwarp();
-      bool lost = member && w.qown[q & 255] != lane;
-      if (__any_sync(FULLMASK, lost)) {
-        unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
-        bool multi = member && __popc(gm) > 1;
-        unsigned um = __ballot_sync(FULLMASK, multi);
-        while (um) {
-          int j = __ffs(um) - 1;
-          um &= um - 1;
-          unsigned long long hj = __shfl_sync(FULLMASK, h, j), kj = __shfl_sync(FULLMASK, k, j);
-          if (multi && (gm >> j & 1) && (hj < h || (hj == h && kj < k))) ++myrank;
-        }
-        maxrank = (int)__reduce_max_sync(FULLMASK, (unsigned)myrank);
-      }
+      // origin) order.  A 64-bin queue hash rules out shared queues in the
+      // common case; otherwise the members of each shared queue rank themselves.
+      TC(3);
       bool win = member;
       unsigned wb = __ballot_sync(FULLMASK, win);
       nw = __popc(wb);
-      if (win && w.flags[0]) { w.qbest[q] = ~0ull; w.qready[q] = ~0ull; }  // bid left by a capped slow round
+      unsigned hlo = __reduce_or_sync(FULLMASK, (member && !(q & 32)) ? 1u << (q & 31) : 0u);
+      unsigned hhi = __reduce_or_sync(FULLMASK, (member && (q & 32)) ? 1u << (q & 31) : 0u);
+      TC(4);
+      if (__popc(hlo) + __popc(hhi) < nw) {
+        unsigned gm = __match_any_sync(FULLMASK, member ? q : (0x40000000 | lane));
+        unsigned others = member ? (gm & ~(1u << lane)) : 0u;
+        int cnt = __popc(others);
+        maxrank = (int)__reduce_max_sync(FULLMASK, (unsigned)cnt);
+        for (int j = 0; j < maxrank; ++j) {
+          int src = others ? __ffs(others) - 1 : lane;
+          others &= others - 1;
+          unsigned long long hj = __shfl_sync(FULLMASK, h, src), kj = __shfl_sync(FULLMASK, k, src);
+          if (j < cnt && (hj < h || (hj == h && kj < k))) ++myrank;
+        }
+      }
+      TC(5);
+      if (win && dirty) { w.qbest[q] = ~0ull; w.qready[q] = ~0ull; }  // bid left by a capped slow round
       bool keep = valid && !win;
       unsigned kb = __ballot_sync(FULLMASK, keep);
       if (keep) {
@@ -918,9 +946,11 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       mine = win;
       if (win) w.wlane[__popc(wb & ((1u << lane) - 1u))] = lane;
       mykey = k; myready = r; myexe = e; myq = q;
+      TC(6);
       PH_ADD(15, t_cl);
     } else {
       if (lane == 0) w.flags[0] = 1;
+      dirty = true;
       // ---- scan 1: minimum key and LB = min(ready + exe)
       unsigned long long bh = ~0ull, bl = ~0ull, lb = INF_BITS;
       for (int i = lane; i < n; i += 32) {
@@ -1040,6 +1070,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
     }
     PH_ADD(2, t_sel);
+    TC(7);
     PH_CNT(13, nw);
     PH_T(t_succ);
     // ---- successors: lane groups of G per winner, random access into each list.
@@ -1061,6 +1092,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int wrec = __shfl_sync(FULLMASK, myrec, srcl);
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
     const bool fwd = kind == KIND_OP;
+    TC(10);
     const int *poff = fwd ? T.op_out_off : T.op_in_off;
     const int *plist = fwd ? T.op_out_pairs : T.op_in_pairs;
     const int *pbase = fwd ? w.prow : w.pcol;
@@ -1077,10 +1109,29 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       if (fwd || kind == KIND_OP_BWD) {
         wdev = w.asg[T.op_slot_off[a] + c];
         int r0 = j0;
-        for (int i = poff[a]; i < poff[a + 1]; ++i) {
+        int i0 = poff[a], np = poff[a + 1] - i0;
+        // the first four pairs: loads issued together (three dependent steps in all)
+        int pp[4], ix[4], ea0[4], ea1[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pp[j] = j < np ? plist[i0 + j] : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ix[j] = j < np ? pbase[pp[j]] + c : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          ea0[j] = j < np ? eoff[ix[j]] : 0;
+          ea1[j] = j < np ? eoff[ix[j] + 1] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int len = ea1[j] - ea0[j];
+          if (fe < 0 && r0 >= 0 && r0 < len) { fe = ea0[j] + r0; fp = pp[j]; }
+          r0 -= len;
+          L += len;
+        }
+        for (int i = i0 + 4; i < i0 + np; ++i) {
           int p = plist[i];
-          int ix = pbase[p] + c;
-          int e0 = eoff[ix], len = eoff[ix + 1] - e0;
+          int x = pbase[p] + c;
+          int e0 = eoff[x], len = eoff[x + 1] - e0;
           if (fe < 0 && r0 >= 0 && r0 < len) { fe = e0 + r0; fp = p; }
           r0 -= len;
           L += len;
@@ -1107,11 +1158,13 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     }
     Ent32 fen;
     fen.kl = 0; fen.pad = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
+    TC(11);
     if (fe >= 0) fen = etab[fe];
     int Lt = L + (fact ? 1 : 0);
     int iters = (Lt + G - 1) >> lgG;
     iters = (int)__reduce_max_sync(FULLMASK, (unsigned)(act_lane ? iters : 0));
     PH_ADD(3, t_succ);
+    TC(8);
     PH_CNT(14, iters);
     PH_T(t_it);
     for (int t = 0; t < iters; ++t) {
@@ -1156,23 +1209,40 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       } else if (act_lane && idx == L && fact) {
         act = fact; slot = fslot; skey = fkey; pq = fq; pexe = fexe; err = ferr; ea = fea; eb = feb;
       }
+      if (t == 0) TC(12);
       if (w.tr && act != 0 && wrec >= 0) {
         int e_ = atomicAdd(w.tr->n_edges, 1);
         if (e_ < w.tr->edge_cap) { w.tr->edge_pred[e_] = wrec; w.tr->edge_succ[e_] = skey; }
       }
-      // arrivals: every max lands before any count reaches zero (the warp
-      // barrier orders them); the u16 counter is decremented through the
-      // 32-bit word that holds it (no borrow: it stops at zero)
-      if (act == 1) atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(wend));
-      __syncwarp();
+      // arrivals.  The u16 counter is decremented through the 32-bit word that
+      // holds it (no borrow: it stops at zero).  When no two lanes arrive at one
+      // counter in this iteration (a 64-bin hash says so), each arriver folds
+      // its end into the ready time itself: the last one keeps the maximum,
+      // the others store it.  Otherwise every max lands (atomically) before
+      // any count is taken, ordered by the warp barrier.
+      bool arr = act == 1;
+      unsigned alo = __reduce_or_sync(FULLMASK, (arr && !(slot & 32)) ? 1u << (slot & 31) : 0u);
+      unsigned ahi = __reduce_or_sync(FULLMASK, (arr && (slot & 32)) ? 1u << (slot & 31) : 0u);
+      bool shared_slot = __popc(alo) + __popc(ahi) < __popc(__ballot_sync(FULLMASK, arr));
+      if (shared_slot) {
+        if (arr) atomicMax((unsigned long long *)&st.ready[slot], (unsigned long long)__double_as_longlong(wend));
+        __syncwarp();
+      }
+      if (t == 0) TC(13);
       bool want = false;
       double pready = 0.0;
-      if (act == 1) {
+      if (arr) {
         unsigned sh = (slot & 1) * 16;
         unsigned old = atomicSub((unsigned *)(st.rem + (slot & ~1)), 1u << sh);
-        if (((old >> sh) & 0xffffu) == 1u) {
+        bool last = ((old >> sh) & 0xffffu) == 1u;
+        double cur = st.ready[slot];
+        if (!shared_slot) {
+          if (wend > cur) cur = wend;
+          if (!last) st.ready[slot] = cur;
+        }
+        if (last) {
           want = true;
-          pready = st.ready[slot];
+          pready = cur;
           unsigned sk = key_kind(skey);
           if (sk == KIND_SYNC) {
             if (!sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb)) err = true;
@@ -1184,6 +1254,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         want = true;
         pready = wend;
       }
+      if (t == 0) TC(14);
       unsigned bad = __ballot_sync(FULLMASK, err);
       if (bad) {
         int s3 = __ffs(bad) - 1;
@@ -1196,6 +1267,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       __syncwarp();
     }
     PH_ADD(4, t_it);
+    TC(9);
+#ifdef PS_TCYC
+    ++tc_r;
+#endif
     __syncwarp();
   }
   // makespan: max over lanes
@@ -2167,6 +2242,20 @@ int ps_mcmc_stop(ps_mcmc *m, const uint8_t *stop) {
 
 
 int ps_mcmc_chains(const ps_mcmc *m) { return m ? m->n : 0; }
+
+int ps_debug_tcyc(long long *out) {
+#ifdef PS_TCYC
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, g_tc, sizeof(long long) * 4096 * 16));
+  int ns = 0;
+  CK(cudaMemcpyFromSymbol(&ns, g_tc_sim, sizeof(int)));
+  fprintf(stderr, "[parasim] tcyc: %d simulations on warp 0\n", ns);
+  return PS_OK;
+#else
+  (void)out;
+  return fail(PS_ERR_INVALID, "built without PS_TCYC");
+#endif
+}
 
 int ps_debug_phases(unsigned long long *out, int reset) {
 #ifdef PS_PHASES
