@@ -888,6 +888,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     double myready = 0.0, myexe = 0.0;
     int myq = -1;
     int myrank = 0, maxrank = 0;  // position among this round's members on the same queue
+    double end = 0.0, mystart = 0.0;
+    bool ran = false;  // fast path: rank-0 members already ran (their queue clock is the one read this round)
     if (n <= 32) {
       // ---- fast path: entry `lane` lives in this lane's registers for the round
       bool valid = lane < n;
@@ -946,6 +948,14 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       mine = win;
       if (win) w.wlane[__popc(wb & ((1u << lane) - 1u))] = lane;
       mykey = k; myready = r; myexe = e; myq = q;
+      if (win && myrank == 0) {
+        // the first member on its queue starts at max(ready, clock) with the
+        // clock read above: end = el (simulate.py:92-94)
+        mystart = r < ck ? ck : r;
+        end = el;
+        w.qclock[q] = end;
+      }
+      ran = true;
       TC(6);
       PH_ADD(15, t_cl);
     } else {
@@ -1041,9 +1051,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       mine = lane < nw;
       w.wlane[lane] = lane;
     }
-    // ---- run the winners: distinct queues, each its queue's next task
-    double end = 0.0, mystart = 0.0;
-    for (int lv = 0; lv <= maxrank; ++lv) {
+    // ---- run the winners: per queue in (ready, origin) order
+    for (int lv = ran ? 1 : 0; lv <= maxrank; ++lv) {
+      if (ran) __syncwarp();
       if (mine && myrank == lv) {
         double clk = w.qclock[myq];
         double start = myready < clk ? clk : myready;
@@ -1051,7 +1061,6 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         end = start + myexe;
         w.qclock[myq] = end;
       }
-      if (maxrank) __syncwarp();
     }
     if (mine) {
       if (end > out.makespan) out.makespan = end;
@@ -1090,6 +1099,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     unsigned long long wkey = __shfl_sync(FULLMASK, mykey, srcl);
     double wend = __shfl_sync(FULLMASK, end, srcl);
     int wrec = __shfl_sync(FULLMASK, myrec, srcl);
+    int wq = __shfl_sync(FULLMASK, myq, srcl);  // an operator task's queue is its device
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
     const bool fwd = kind == KIND_OP;
     TC(10);
@@ -1107,7 +1117,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     bool ferr = false;
     if (act_lane) {
       if (fwd || kind == KIND_OP_BWD) {
-        wdev = w.asg[T.op_slot_off[a] + c];
+        wdev = wq;
         int r0 = j0;
         int i0 = poff[a], np = poff[a + 1] - i0;
         // the first four pairs: loads issued together (three dependent steps in all)
@@ -1136,19 +1146,21 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           r0 -= len;
           L += len;
         }
-        if (fwd) {
-          if (P.full) { fact = 1; fslot = Tf + w.fbase[a] + c; fkey = pack_key(KIND_OP_BWD, a, 0, c, 0); }
-        } else if (T.op_param_mask[a] >= 0) {
+        if (!fwd && T.op_param_mask[a] >= 0) {
           int si = st.grp[w.fbase[a] + c];
           if (__popcll((long long)st.gmask[w.gbase[a] + si]) >= 2) {
             fact = 1; fslot = 2 * Tf + w.gbase[a] + si; fkey = pack_key(KIND_SYNC, a, si, 0, 0);
           }
         }
-      } else if (kind == KIND_EDGE) {
-        fact = 1; fslot = w.fbase[b] + d; fkey = pack_key(KIND_OP, b, 0, d, 0);
-      } else if (kind == KIND_EDGE_BWD) {
-        fact = 1; fslot = Tf + w.fbase[a] + c; fkey = pack_key(KIND_OP_BWD, a, 0, c, 0);
-      } else {  // ring hop c -> c + 1 (none after the last)
+      }
+      if ((fwd && P.full) || kind == KIND_EDGE || kind == KIND_EDGE_BWD) {
+        // forward -> its backward task; transfer -> the task it feeds
+        bool tf = kind == KIND_EDGE;
+        int xo = tf ? (int)b : (int)a, xb = tf ? (int)d : (int)c;
+        fact = 1;
+        fslot = (tf ? 0 : Tf) + w.fbase[xo] + xb;
+        fkey = pack_key(tf ? KIND_OP : KIND_OP_BWD, xo, 0, xb, 0);
+      } else if (kind == KIND_SYNC) {  // ring hop c -> c + 1 (none after the last)
         int r = __popcll((long long)st.gmask[w.gbase[a] + b]);
         if ((int)c + 1 < 2 * (r - 1)) {
           fact = 2; fkey = pack_key(KIND_SYNC, a, b, c + 1, 0);
