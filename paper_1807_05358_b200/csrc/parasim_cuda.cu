@@ -535,6 +535,7 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
   return w;
 }
 
+template <bool TR>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
 
 // Simulate; a candidate whose ready set outgrows shared memory is re-run with
@@ -546,7 +547,7 @@ __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &
   W2 wg = w;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    o = warp_simulate2(P, T, wg, L, gscratch, lane);
+    o = warp_simulate2<false>(P, T, wg, L, gscratch, lane);
     if (o.status != PS_STATUS_CAPACITY) break;
     wg = with_global_ready_set(P, gscratch, w);
   }
@@ -786,6 +787,9 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
   return 0.0;
 }
 
+// TR: record every task and dependency (k_simulate_trace); compiled out of the
+// evaluation kernels
+template <bool TR>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   SimOut out;
   out.makespan = 0.0;
@@ -1052,6 +1056,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       w.wlane[lane] = lane;
     }
     // ---- run the winners: per queue in (ready, origin) order
+#pragma unroll 1
     for (int lv = ran ? 1 : 0; lv <= maxrank; ++lv) {
       if (ran) __syncwarp();
       if (mine && myrank == lv) {
@@ -1068,7 +1073,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         atomicMin((unsigned long long *)&w.opmin[key_a(mykey)], (unsigned long long)__double_as_longlong(end));
     }
     int myrec = -1;
-    if (w.tr && mine) {
+    if (TR && w.tr && mine) {
       myrec = atomicAdd(w.tr->n_tasks, 1);
       if (myrec < w.tr->task_cap) {
         ps_trace_task rec;
@@ -1222,7 +1227,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         act = fact; slot = fslot; skey = fkey; pq = fq; pexe = fexe; err = ferr; ea = fea; eb = feb;
       }
       if (t == 0) TC(12);
-      if (w.tr && act != 0 && wrec >= 0) {
+      if (TR && w.tr && act != 0 && wrec >= 0) {
         int e_ = atomicAdd(w.tr->n_edges, 1);
         if (e_ < w.tr->edge_cap) { w.tr->edge_pred[e_] = wrec; w.tr->edge_succ[e_] = skey; }
       }
@@ -1345,11 +1350,11 @@ k_simulate_trace(DevProb P, Lay lay, const int *map, const unsigned char *asg, c
     for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = asg[i];
   w.tr = &tr;
   __syncwarp();
-  SimOut o = warp_simulate2(P, T, w, lay, gscratch, lane);
+  SimOut o = warp_simulate2<true>(P, T, w, lay, gscratch, lane);
   if (o.status == PS_STATUS_CAPACITY) {  // wide ready set: rerun in global memory, fresh trace
     if (lane == 0) { *tr.n_tasks = 0; *tr.n_edges = 0; }
     __syncwarp();
-    o = warp_simulate2(P, T, with_global_ready_set(P, gscratch, w), lay, gscratch, lane);
+    o = warp_simulate2<true>(P, T, with_global_ready_set(P, gscratch, w), lay, gscratch, lane);
   }
   if (lane == 0) {
     *makespan = o.makespan;
