@@ -535,11 +535,16 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
   return w;
 }
 
-template <bool TR>
+// simulator variants: SIM_TRACE records every task and dependency
+// (k_simulate_trace), SIM_OPMIN keeps each op's earliest forward end (exhaustive
+// search bounds); the MCMC kernel compiles neither
+enum { SIM_TRACE = 1, SIM_OPMIN = 2 };
+template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
 
 // Simulate; a candidate whose ready set outgrows shared memory is re-run with
 // the ready set in global memory (same answer, slower).
+template <int M>
 __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch,
                                       int lane) {
   // one inlined copy of the simulator per call site (the code is large: keep it in the instruction cache)
@@ -547,7 +552,7 @@ __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &
   W2 wg = w;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    o = warp_simulate2<false>(P, T, wg, L, gscratch, lane);
+    o = warp_simulate2<M>(P, T, wg, L, gscratch, lane);
     if (o.status != PS_STATUS_CAPACITY) break;
     wg = with_global_ready_set(P, gscratch, w);
   }
@@ -695,6 +700,11 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
   return st;
 }
 
+// IEEE division out of line: the transfer-time and ring-hop divisions sit on
+// rare paths of the simulator loop, whose code must stay small for the
+// instruction cache (by value only: nothing is forced to local memory)
+__device__ __noinline__ double div_rn(double a, double b) { return a / b; }
+
 // exe time / queue of a transfer between devices da -> db carrying nb bytes
 __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int da, int db, double nb, int &q,
                                            double &exe) {
@@ -702,10 +712,10 @@ __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int d
   if (lv < 0) return false;
   if (P.n_cls) {
     q = P.n_dev + (lv & 0x3fff);
-    exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + nb / ((lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
+    exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + div_rn(nb, (lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
   } else {
     q = P.n_dev + lv;
-    exe = __ldg(&T.link_lat[lv]) + nb / __ldg(&T.link_bw[lv]);
+    exe = __ldg(&T.link_lat[lv]) + div_rn(nb, __ldg(&T.link_bw[lv]));
   }
   return true;
 }
@@ -729,7 +739,7 @@ __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const
   // kept in the ring's counter slot, which is free from then on
   double *per = &st.ready[2 * st.Tf + gi];
   double nb;
-  if (hop == 0) { nb = P.map_shard[w.gmap[a]] / (double)r; *per = nb; }
+  if (hop == 0) { nb = div_rn(P.map_shard[w.gmap[a]], (double)r); *per = nb; }
   else nb = *per;
   if (!link_attrs(P, T, da, db, nb, q, exe)) { ea = da; eb = db; return false; }
   if (hop + 1 >= 2 * (r - 1)) q |= Q_SINK;
@@ -787,9 +797,7 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
   return 0.0;
 }
 
-// TR: record every task and dependency (k_simulate_trace); compiled out of the
-// evaluation kernels
-template <bool TR>
+template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   SimOut out;
   out.makespan = 0.0;
@@ -1069,11 +1077,11 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     }
     if (mine) {
       if (end > out.makespan) out.makespan = end;
-      if (w.opmin && key_kind(mykey) == KIND_OP)
+      if ((M & SIM_OPMIN) && key_kind(mykey) == KIND_OP)
         atomicMin((unsigned long long *)&w.opmin[key_a(mykey)], (unsigned long long)__double_as_longlong(end));
     }
     int myrec = -1;
-    if (TR && w.tr && mine) {
+    if ((M & SIM_TRACE) && mine) {
       myrec = atomicAdd(w.tr->n_tasks, 1);
       if (myrec < w.tr->task_cap) {
         ps_trace_task rec;
@@ -1227,7 +1235,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         act = fact; slot = fslot; skey = fkey; pq = fq; pexe = fexe; err = ferr; ea = fea; eb = feb;
       }
       if (t == 0) TC(12);
-      if (TR && w.tr && act != 0 && wrec >= 0) {
+      if ((M & SIM_TRACE) && act != 0 && wrec >= 0) {
         int e_ = atomicAdd(w.tr->n_edges, 1);
         if (e_ < w.tr->edge_cap) { w.tr->edge_pred[e_] = wrec; w.tr->edge_succ[e_] = skey; }
       }
@@ -1324,7 +1332,7 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
       for (int i = lane; i < P.n_ops; i += 32) w.opmin[i] = __longlong_as_double(0x7ff0000000000000ll);
     }
     __syncwarp();
-    SimOut o = simulate_any(P, T, w, lay, gs, lane);
+    SimOut o = opmin ? simulate_any<SIM_OPMIN>(P, T, w, lay, gs, lane) : simulate_any<0>(P, T, w, lay, gs, lane);
     if (lane == 0) {
       makespan[cand] = o.status == PS_STATUS_OK ? o.makespan : -1.0;
       status[cand] = o.status;
@@ -1350,11 +1358,11 @@ k_simulate_trace(DevProb P, Lay lay, const int *map, const unsigned char *asg, c
     for (int i = lane; i < P.n_slots; i += 32) w.asg[i] = asg[i];
   w.tr = &tr;
   __syncwarp();
-  SimOut o = warp_simulate2<true>(P, T, w, lay, gscratch, lane);
+  SimOut o = warp_simulate2<SIM_TRACE>(P, T, w, lay, gscratch, lane);
   if (o.status == PS_STATUS_CAPACITY) {  // wide ready set: rerun in global memory, fresh trace
     if (lane == 0) { *tr.n_tasks = 0; *tr.n_edges = 0; }
     __syncwarp();
-    o = warp_simulate2<true>(P, T, with_global_ready_set(P, gscratch, w), lay, gscratch, lane);
+    o = warp_simulate2<SIM_TRACE>(P, T, with_global_ready_set(P, gscratch, w), lay, gscratch, lane);
   }
   if (lane == 0) {
     *makespan = o.makespan;
@@ -1594,7 +1602,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     if (same) {
       cand = cs.cost;
     } else {
-      SimOut so = simulate_any(P, T, w, lay, gs, lane);
+      SimOut so = simulate_any<0>(P, T, w, lay, gs, lane);
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
         if (it < 0) {
