@@ -700,11 +700,6 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
   return st;
 }
 
-// IEEE division out of line: the transfer-time and ring-hop divisions sit on
-// rare paths of the simulator loop, whose code must stay small for the
-// instruction cache (by value only: nothing is forced to local memory)
-__device__ __noinline__ double div_rn(double a, double b) { return a / b; }
-
 // exe time / queue of a transfer between devices da -> db carrying nb bytes
 __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int da, int db, double nb, int &q,
                                            double &exe) {
@@ -712,10 +707,10 @@ __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int d
   if (lv < 0) return false;
   if (P.n_cls) {
     q = P.n_dev + (lv & 0x3fff);
-    exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + div_rn(nb, (lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
+    exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + nb / ((lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
   } else {
     q = P.n_dev + lv;
-    exe = __ldg(&T.link_lat[lv]) + div_rn(nb, __ldg(&T.link_bw[lv]));
+    exe = __ldg(&T.link_lat[lv]) + nb / __ldg(&T.link_bw[lv]);
   }
   return true;
 }
@@ -739,7 +734,7 @@ __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const
   // kept in the ring's counter slot, which is free from then on
   double *per = &st.ready[2 * st.Tf + gi];
   double nb;
-  if (hop == 0) { nb = div_rn(P.map_shard[w.gmap[a]], (double)r); *per = nb; }
+  if (hop == 0) { nb = P.map_shard[w.gmap[a]] / (double)r; *per = nb; }
   else nb = *per;
   if (!link_attrs(P, T, da, db, nb, q, exe)) { ea = da; eb = db; return false; }
   if (hop + 1 >= 2 * (r - 1)) q |= Q_SINK;
