@@ -300,3 +300,48 @@ def test_global_memory_layouts(oracle, monkeypatch, hook):
     ref = oracle.mcmc(g, topo, prof, mode, init, [7 + 1000003 * c for c in range(3)], 80, md, rng_mode="philox")
     for ci, ch in enumerate(rep.chains):
         assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted) == tuple(ref["summary"][ci][:4])
+
+
+# ---------------------------------------------------------------- full sizes
+# BASELINE.json configs at their own sizes (not reduced): the GPU path against
+# the oracle, strategy by strategy, and the 1024-chain MCMC the bench times.
+
+def _full_size_cases():
+    return [
+        ("resnet101_16x4", ps.resnet101(), ps.multi_node_topology(16, 4), 8),
+        ("nmt40_16x4", ps.nmt_like(steps=40, layers=2, batch=64, hidden=1024, vocab=32768),
+         ps.multi_node_topology(16, 4), 8),
+        ("random1k_4x4", ps.random_dag(1000, seed=1000), ps.multi_node_topology(4, 4), 4),
+    ]
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_full_size_configs_match_oracle(oracle, case):
+    name, g, topo, md = _full_size_cases()[case]
+    prof = ps.CostProfile()
+    strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, s) for s in range(3)]
+    for mode in (ps.MODE_FULL, ps.MODE_FORWARD):
+        got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=md)
+        want = oracle.makespans(g, topo, prof, mode, strategies)
+        assert list(got) == list(want), (name, mode)
+
+
+def test_bench_config_mcmc_matches_oracle(oracle):
+    """Inception-v3 on 4x4 devices, full-iteration, 1024 chains (the bench
+    workload, Philox streams): every chain's summary and best strategy."""
+    import os
+    g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
+    prof = ps.CostProfile()
+    C, P = 1024, 6
+    init = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, c) for c in range(1, C)]
+    seeds = [1000003 * c for c in range(C)]
+    params = ps.SearchParams(max_proposals=P, seed=0, max_degree=md, mode=ps.MODE_FULL, initial=init,
+                             polish=False, rng="philox")
+    rep = ps.mcmc_search(g, topo, prof, params)
+    ref = oracle.mcmc(g, topo, prof, ps.MODE_FULL, init, seeds, P, md, rng_mode="philox",
+                      threads=os.cpu_count() or 1)
+    got = [(ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted, ch.beta) for ch in rep.chains]
+    want = [tuple(s[:5]) for s in ref["summary"]]
+    assert got == want
+    cand = np.array([c for _, c, _ in rep.trace]).reshape(C, P)
+    assert np.array_equal(cand, ref["cand"])
