@@ -69,11 +69,11 @@ def workload(name, ops=1000):
 
 
 def initial_strategies(g, topo, md, first, count):
+    """[data_parallel] + [random_strategy(seed=c) for c in 1..]: chain c's start."""
     import paper_1807_05358_b200 as ps
-    out = []
-    for c in range(first, first + count):
-        out.append(ps.data_parallel_strategy(g, topo) if c == 0 else ps.random_strategy(g, topo, md, c))
-    return out
+    seeds = [c for c in range(first, first + count) if c != 0]
+    rand = iter(ps.random_strategies(g, topo, md, seeds))
+    return [ps.data_parallel_strategy(g, topo) if c == 0 else next(rand) for c in range(first, first + count)]
 
 
 class ClockSampler:

@@ -42,12 +42,25 @@ MODE_FULL = "full-iteration"
 KIND_NAMES = ("edge", "edge_bwd", "op", "op_bwd", "sync")
 
 
+_DEGREE_TUPLES: dict = {}
+
+
 def degree_tuple(op, degrees: dict) -> tuple[int, ...]:
+    """Degrees in output-dim order (missing dims = 1); memoised on the (frozen)
+    output shape and the degree items, since large searches look the same few
+    maps up millions of times."""
+    key = (op.output_shape.dims, tuple(degrees.items()))
+    hit = _DEGREE_TUPLES.get(key)
+    if hit is not None:
+        return hit
     names = op.output_shape.names()
     for n in degrees:
         if n not in names:
             raise ValueError(f"op {op.id}: degree given for dimension {n} absent from its output")
-    return tuple(int(degrees.get(n, 1)) for n in names)
+    t = tuple(int(degrees.get(n, 1)) for n in names)
+    if len(_DEGREE_TUPLES) < 1 << 16:
+        _DEGREE_TUPLES[key] = t
+    return t
 
 
 @dataclass
@@ -233,11 +246,14 @@ def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree
             lst = [degree_tuple(op, c.degrees) for c in enumerate_configs(op, topo, max_degree)]
         n_enum.append(len(lst))
         idx = {t: i for i, t in enumerate(lst)}
+        seen = {}  # id(degrees dict) -> tuple: batched strategies share their dicts
         for s in strategies:
             cfg = s.configs.get(oid)
             if cfg is None:
                 continue
-            t = degree_tuple(op, cfg.degrees)
+            t = seen.get(id(cfg.degrees))
+            if t is None:
+                t = seen[id(cfg.degrees)] = degree_tuple(op, cfg.degrees)
             if t not in idx:
                 grid_of(op, ParallelizationConfig(dict(zip(op.output_shape.names(), t))))  # divisibility
                 idx[t] = len(lst)

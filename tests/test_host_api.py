@@ -272,3 +272,13 @@ def test_product_path_has_no_cpu_fallback(monkeypatch):
     topo = ps.single_node_topology(gpus=4)
     with pytest.raises(nat.NativeUnavailable):
         ps.build_task_graph(g, topo, ps.data_parallel_strategy(g, topo), ps.CostProfile())
+
+
+def test_random_strategies_batch_equals_single_draws():
+    g, topo = ps.inception_v3(), ps.multi_node_topology(4, 4)
+    seeds = [0, 1, 17, 1000003]
+    batch = ps.random_strategies(g, topo, 4, seeds)
+    for s, b in zip(seeds, batch):
+        one = ps.random_strategy(g, topo, 4, s)
+        assert {k: (c.degrees, c.assignment) for k, c in one.configs.items()} == \
+            {k: (c.degrees, c.assignment) for k, c in b.configs.items()}
