@@ -324,6 +324,36 @@ def run_ours(args):
         dist.all_reduce(e2e_n, op=dist.ReduceOp.SUM)
     e2e_value = float(e2e_n.item()) / float(e2e_t.item())
 
+    # ---- full evaluation (build + full simulate, no search): the chains' current
+    # strategies scored in one k_simulate_batch launch per step, device-resident
+    # (8 candidates per chain and launch, so the launch is not paced by its slowest candidate)
+    FB = 8 * C
+    fmaps = torch.from_numpy(np.repeat(sm, 8, axis=0)).to(dev)
+    fasg = torch.from_numpy(np.repeat(sa, 8, axis=0)).to(dev)
+    fmk = torch.empty(FB, dtype=torch.float64, device=dev)
+    fst = torch.empty(FB, dtype=torch.int32, device=dev)
+
+    def full_step():
+        nat.check(L.ps_simulate_batch(low.handle(), ctypes.c_void_p(fmaps.data_ptr()), ctypes.c_void_p(fasg.data_ptr()),
+                                      FB, ctypes.c_void_p(fmk.data_ptr()), ctypes.c_void_p(fst.data_ptr()),
+                                      nat.PS_DEVICE_PTRS, sh), "ps_simulate_batch")
+
+    for _ in range(args.warmup):
+        full_step()
+    torch.cuda.synchronize(dev)
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a_, b_ in fev:
+        a_.record(stream)
+        full_step()
+        b_.record(stream)
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+    torch.cuda.synchronize(dev)
+    f_ms = torch.tensor([sum(a_.elapsed_time(b_) for a_, b_ in fev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(f_ms, op=dist.ReduceOp.MAX)
+    full_value = world * FB * args.steps / (float(f_ms.item()) / 1e3)
+    bad_full = int((fst != nat.PS_STATUS_OK).sum().item())
+
     peak, peak_src = measured_peak()
     achieved = bytes_per_eval * (evals / (total_ms / 1e3)) / 1e9  # this rank's kernel, GB/s
     tpe = profiled_traffic_per_eval()
@@ -350,6 +380,9 @@ def run_ours(args):
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
         "chain_failures": bad, "best_makespan": float(best.item()), "best_chain": win_chain,
+        "full_eval": {"value": full_value, "unit": UNIT, "candidates_per_launch": FB, "failures": bad_full,
+                      "note": "full evaluations (no search) of the chains' current strategies (8 adjacent copies each), "
+                              "one k_simulate_batch launch per step, device-resident inputs"},
     }
     L.ps_mcmc_destroy(h)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1303,10 +1303,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 
 __global__ void __launch_bounds__(256, 1)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
-                 double *makespan, int *status, char *gscratch, double *opmin) {
+                 double *makespan, int *status, char *gscratch, double *opmin, int *next) {
   extern __shared__ __align__(16) char smem[];
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
+  int gw = blockIdx.x * wpb + wib;
   char *gs = gscratch + (size_t)gw * gslice_bytes(P, lay);
   Tab T;
   W2 w;
@@ -1315,7 +1315,10 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
   bind_bids(P, gs, w);
   if (lane == 0) w.flags[0] = 1;  // the global bid arrays start uninitialised
   __syncwarp();
-  for (int cand = gw; cand < n; cand += nw) {
+  // candidates are taken from a work queue: a slow one (e.g. a wide data-parallel
+  // strategy) holds up only its own warp
+  for (int cand = __shfl_sync(FULLMASK, lane == 0 ? atomicAdd(next, 1) : 0, 0); cand < n;
+       cand = __shfl_sync(FULLMASK, lane == 0 ? atomicAdd(next, 1) : 0, 0)) {
     const int *m = maps + (size_t)cand * P.n_ops;
     const unsigned char *a = asgs + (size_t)cand * P.n_slots;
     for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = m[i];
@@ -1716,6 +1719,7 @@ struct ps_problem {
   unsigned char *d_asg = nullptr;
   double *d_mk = nullptr;
   int *d_st = nullptr;
+  int *d_next = nullptr;  // batch work queue: next candidate to take
   size_t io_cap = 0;
   long long device_bytes = 0;
 };
@@ -1964,7 +1968,7 @@ void ps_problem_destroy(ps_problem *pr) {
   cudaSetDevice(pr->device);
   for (void *p : pr->owned) cudaFree(p);
   cudaFree(pr->scratch);
-  cudaFree(pr->d_map); cudaFree(pr->d_asg); cudaFree(pr->d_mk); cudaFree(pr->d_st);
+  cudaFree(pr->d_map); cudaFree(pr->d_asg); cudaFree(pr->d_mk); cudaFree(pr->d_st); cudaFree(pr->d_next);
   delete pr;
 }
 
@@ -2043,7 +2047,10 @@ int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t
     if (flags == PS_DEVICE_PTRS) dop = op_min_end_out;
     else CK(cudaMalloc(&dop, (size_t)n * pr->P.n_ops * sizeof(double)));
   }
-  k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop);
+  if (!pr->d_next) CK(cudaMalloc(&pr->d_next, sizeof(int)));
+  CK(cudaMemsetAsync(pr->d_next, 0, sizeof(int), s));
+  k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop,
+                                                                 pr->d_next);
   CK(cudaGetLastError());
   if (flags != PS_DEVICE_PTRS) {
     CK(cudaMemcpyAsync(makespan_out, dk, n * sizeof(double), cudaMemcpyDeviceToHost, s));
