@@ -897,12 +897,45 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int myrank = 0, maxrank = 0;  // position among this round's members on the same queue
     double end = 0.0, mystart = 0.0;
     bool ran = false;  // fast path: rank-0 members already ran (their queue clock is the one read this round)
-    if (n <= 32) {
+    // Medium path (33..64 ready tasks, two per lane): when the round's members
+    // are at most 32, they are staged at [64, 64 + members) and the others
+    // compacted to [0, rest); the fast path below then runs the members alone.
+    int sel_base = 0, sel_n = n, rest = 0;
+    bool forced = false;
+    if (n > 32 && n <= 64 && n + 32 <= w.rcap) {
+      bool vA = true, vB = lane + 32 < n;
+      unsigned long long hA = w.rhi[lane], kA = w.rlo[lane], hB = vB ? w.rhi[lane + 32] : ~0ull,
+                         kB = vB ? w.rlo[lane + 32] : ~0ull;
+      double eA = w.rexe[lane], eB = vB ? w.rexe[lane + 32] : 0.0;
+      int qA = w.rq[lane], qB = vB ? w.rq[lane + 32] : 0;
+      double rA = __longlong_as_double((long long)hA), rB = __longlong_as_double((long long)hB);
+      double cA = w.qclock[qA & Q_MASK], cB = vB ? w.qclock[qB & Q_MASK] : 0.0;
+      double lA = (rA < cA ? cA : rA) + eA, lB = (rB < cB ? cB : rB) + eB;
+      unsigned long long bA = !(qA & Q_SINK) ? (unsigned long long)__double_as_longlong(lA) : INF_BITS;
+      unsigned long long bB = (vB && !(qB & Q_SINK)) ? (unsigned long long)__double_as_longlong(lB) : INF_BITS;
+      double LB2 = __longlong_as_double((long long)warp_min64(bA < bB ? bA : bB, lane));
+      bool mA = vA && rA < LB2, mB = vB && rB < LB2;
+      unsigned gA = __ballot_sync(FULLMASK, mA), gB = __ballot_sync(FULLMASK, mB);
+      int nm = __popc(gA) + __popc(gB);
+      if (nm > 0 && nm <= 32) {
+        unsigned lt = (1u << lane) - 1u;
+        unsigned xA = __ballot_sync(FULLMASK, vA && !mA), xB = __ballot_sync(FULLMASK, vB && !mB);
+        int pA = mA ? 64 + __popc(gA & lt) : __popc(xA & lt);
+        int pB = mB ? 64 + __popc(gA) + __popc(gB & lt) : __popc(xA) + __popc(xB & lt);
+        __syncwarp();
+        w.rhi[pA] = hA; w.rlo[pA] = kA; w.rexe[pA] = eA; w.rq[pA] = qA;
+        if (vB) { w.rhi[pB] = hB; w.rlo[pB] = kB; w.rexe[pB] = eB; w.rq[pB] = qB; }
+        __syncwarp();
+        sel_base = 64; sel_n = nm; rest = n - nm; forced = true;
+      }
+    }
+    if (sel_n <= 32) {
       // ---- fast path: entry `lane` lives in this lane's registers for the round
-      bool valid = lane < n;
-      unsigned long long h = valid ? w.rhi[lane] : ~0ull, k = valid ? w.rlo[lane] : ~0ull;
-      double e = valid ? w.rexe[lane] : 0.0;
-      int qr = valid ? w.rq[lane] : 0;
+      bool valid = lane < sel_n;
+      int ix = sel_base + lane;
+      unsigned long long h = valid ? w.rhi[ix] : ~0ull, k = valid ? w.rlo[ix] : ~0ull;
+      double e = valid ? w.rexe[ix] : 0.0;
+      int qr = valid ? w.rq[ix] : 0;
       int q = qr & Q_MASK;
       double r = __longlong_as_double((long long)h);
       // LB = min over tasks with successors of max(ready, clock) + exe: no task
@@ -915,7 +948,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       PH_ADD(5, t_sel);
       TC(2);
       PH_T(t_cl);
-      bool member = valid && r < LB;
+      bool member = valid && (forced || r < LB);
       if (!__any_sync(FULLMASK, member)) {
         // degenerate (zero or absorbed exe): the global minimum alone
         int wl = warp_argmin128(h, k, lane);
@@ -951,7 +984,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int pos = __popc(kb & ((1u << lane) - 1u));
         w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = qr;
       }
-      n = __popc(kb);
+      n = forced ? rest : __popc(kb);
       mine = win;
       if (win) w.wlane[__popc(wb & ((1u << lane) - 1u))] = lane;
       mykey = k; myready = r; myexe = e; myq = q;

@@ -43,3 +43,9 @@ for i, n in enumerate(["succ: shfl/decode", "succ: pair walk+fixed", "succ: entr
 tot = t[fast][:, 9] - t[fast][:, 0]
 nxt = t[1:, 0] - t[:-1, 9]
 print(f"round (fast) {tot.mean():.0f} cycles; loop-back {np.median(nxt[nxt > 0]):.0f}")
+ok = (raw[:, 0] > 0) & (raw[:, 9] > raw[:, 0])
+slow = ok & ~fast
+st = raw[slow][:, 9] - raw[slow][:, 0]
+if slow.sum():
+    print(f"slow-path rounds: {slow.sum()} of {ok.sum()}, mean {st.mean():.0f} cycles "
+          f"({100 * st.sum() / (raw[ok][:, 9] - raw[ok][:, 0]).sum():.1f}% of round time)")
