@@ -230,25 +230,28 @@ __global__ void k_cols(DevProb P, int n_cols, int n_combos, int *col_count, cons
   if (!col_off_fill) col_count[q] = cnt;
 }
 
-// 32-byte overlap record: k | l << 16, transfer bytes, and the transfer time
-// on each link class (cost.py:128-130: latency + nbytes / bandwidth)
-struct __align__(16) Ent32 { int kl; int pad; long long bytes; double exe[2]; };
+// 32-byte overlap record: k | l << 16, the task slot of the other end (row
+// order: consumer block l; column order: producer block k), transfer bytes, and
+// the transfer time on each link class (cost.py:128-130: latency + nbytes / bandwidth)
+struct __align__(16) Ent32 { int kl; int slot; long long bytes; double exe[2]; };
 
-__device__ inline Ent32 make_ent(const DevProb &P, int e) {
+__device__ inline Ent32 make_ent(const DevProb &P, int e, int n_rows, int n_combos, bool col) {
   Ent32 r;
   r.kl = (int)((unsigned)P.ent_k[e] | ((unsigned)P.ent_l[e] << 16));
-  r.pad = 0;
+  int row = upper_bound(P.row_ent_off, n_rows + 1, e) - 1;
+  int pr = combo_ref(P, upper_bound(P.combo_row_off, n_combos + 1, row) - 1).p;
+  r.slot = col ? P.op_slot_off[P.pair_src[pr]] + (int)P.ent_k[e] : P.op_slot_off[P.pair_dst[pr]] + (int)P.ent_l[e];
   r.bytes = P.ent_bytes[e];
   for (int c = 0; c < 2; ++c)
     r.exe[c] = c < P.n_cls ? __dadd_rn(P.cls_lat[c], __ddiv_rn((double)r.bytes, P.cls_bw[c])) : 0.0;
   return r;
 }
 
-__global__ void k_pack(DevProb P, int n_ent, void *ent32, void *cent32) {
+__global__ void k_pack(DevProb P, int n_ent, int n_rows, int n_combos, void *ent32, void *cent32) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_ent) return;
-  ((Ent32 *)ent32)[e] = make_ent(P, e);
-  ((Ent32 *)cent32)[e] = make_ent(P, P.col_ent[e]);
+  ((Ent32 *)ent32)[e] = make_ent(P, e, n_rows, n_combos, false);
+  ((Ent32 *)cent32)[e] = make_ent(P, P.col_ent[e], n_rows, n_combos, true);
 }
 
 // ---------------------------------------------------------------- simulator
@@ -1210,7 +1213,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
     }
     Ent32 fen;
-    fen.kl = 0; fen.pad = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
+    fen.kl = 0; fen.slot = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
     TC(11);
     if (fe >= 0) fen = etab[fe];
     int Lt = L + (fact ? 1 : 0);
@@ -1246,7 +1249,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int kk = en.kl & 0xffff, l = en.kl >> 16;
         int xo = fwd ? T.pair_dst[p] : T.pair_src[p];
         int xb = fwd ? l : kk;
-        int xdev = w.asg[T.op_slot_off[xo] + xb];
+        int xdev = w.asg[en.slot];
         if (xdev == wdev) {
           act = 1;
           slot = (fwd ? 0 : Tf) + w.fbase[xo] + xb;
@@ -1908,7 +1911,7 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   CK(cudaMalloc(&c16, (size_t)(n_ent + 1) * sizeof(Ent32)));
   ow.push_back(e16); ow.push_back(c16);
   P.ent16 = e16; P.cent16 = c16;
-  if (n_ent) k_pack<<<(n_ent + 127) / 128, 128>>>(P, n_ent, e16, c16);
+  if (n_ent) k_pack<<<(n_ent + 127) / 128, 128>>>(P, n_ent, (int)n_rows, (int)n_combos, e16, c16);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   cudaFree(cnt); cudaFree(ccnt); cudaFree(tmp);
