@@ -1607,9 +1607,14 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     bool same = false;
     if (it >= 0) {
       ++n_it;
-      if (budget_ns) {  // time-boxed segment: stop between proposals once the budget is spent
+      if (budget_ns) {
+        // time-boxed segment: stop between proposals when the next one (at
+        // this chain's mean proposal time so far) would end past the budget,
+        // so the segment ends close to the budget instead of waiting for the
+        // slowest chain's overshoot
         unsigned long long now = __shfl_sync(FULLMASK, globaltimer_ns(), 0);
-        if (now - t0 >= budget_ns) break;
+        unsigned long long spent = now - t0, mean = n_it > 1 ? spent / (unsigned long long)(n_it - 1) : 0ull;
+        if (spent + mean >= budget_ns) break;
       }
       // _propose_change (search.py:101-115): op, degree map, one device per task
       o = (int)rng.below((unsigned)P.n_ops);
