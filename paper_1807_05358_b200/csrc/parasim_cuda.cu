@@ -1661,8 +1661,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
       for (int i = lane; i < P.n_ops; i += 32) bmap[i] = w.mapl[i];
       for (int i = lane; i < P.n_slots; i += 32) basg[i] = w.asg[i];
       __syncwarp();
-      t0 = globaltimer_ns();
-      continue;
+      continue;  // (the budget covers the initial scoring too: all chains end together)
     }
     long long idx = cs.proposals++;
     bool ok;
@@ -1761,6 +1760,8 @@ struct ps_problem {
   double *d_mk = nullptr;
   int *d_st = nullptr;
   int *d_next = nullptr;  // batch work queue: next candidate to take
+  char *mcmc_scratch = nullptr;  // chain scratch kept from the last destroyed MCMC handle
+  size_t mcmc_scratch_bytes = 0;
   size_t io_cap = 0;
   long long device_bytes = 0;
 };
@@ -1776,6 +1777,7 @@ struct ps_mcmc {
   double *trace_cand;
   unsigned char *trace_ok;
   char *scratch;
+  size_t scratch_bytes = 0;
   double *d_best;
   int *d_bestc;
 };
@@ -2010,6 +2012,7 @@ void ps_problem_destroy(ps_problem *pr) {
   for (void *p : pr->owned) cudaFree(p);
   cudaFree(pr->scratch);
   cudaFree(pr->d_map); cudaFree(pr->d_asg); cudaFree(pr->d_mk); cudaFree(pr->d_st); cudaFree(pr->d_next);
+  cudaFree(pr->mcmc_scratch);
   delete pr;
 }
 
@@ -2221,7 +2224,17 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
   CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
-  CK(cudaMalloc(&m->scratch, (size_t)n * gslice_bytes(P, pr->lay)));
+  {
+    size_t want = (size_t)n * gslice_bytes(P, pr->lay);
+    if (pr->mcmc_scratch && pr->mcmc_scratch_bytes >= want) {  // reuse: repeated create/run/destroy cycles
+      m->scratch = pr->mcmc_scratch;
+      pr->mcmc_scratch = nullptr;
+      m->scratch_bytes = pr->mcmc_scratch_bytes;
+    } else {
+      CK(cudaMalloc(&m->scratch, want));
+      m->scratch_bytes = want;
+    }
+  }
   CK(cudaMalloc(&m->d_best, sizeof(double)));
   CK(cudaMalloc(&m->d_bestc, sizeof(int)));
   CK(cudaMemcpy(m->maps, init_map, (size_t)n * P.n_ops * sizeof(int), cudaMemcpyHostToDevice));
@@ -2363,7 +2376,16 @@ void ps_mcmc_destroy(ps_mcmc *m) {
   if (!m) return;
   cudaSetDevice(m->prob->device);
   cudaFree(m->maps); cudaFree(m->best_maps); cudaFree(m->asgs); cudaFree(m->best_asgs); cudaFree(m->st);
-  cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok); cudaFree(m->scratch);
+  cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok);
+  if (m->scratch) {  // keep the largest chain scratch for the problem's next handle
+    if (m->scratch_bytes >= m->prob->mcmc_scratch_bytes) {
+      cudaFree(m->prob->mcmc_scratch);
+      m->prob->mcmc_scratch = m->scratch;
+      m->prob->mcmc_scratch_bytes = m->scratch_bytes;
+    } else {
+      cudaFree(m->scratch);
+    }
+  }
   cudaFree(m->d_best); cudaFree(m->d_bestc);
   delete m;
 }
