@@ -194,8 +194,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PS_BENCH_BACKEND=gloo lets the N>1 path be exercised with ranks sharing one
+    # GPU (a test hook; the driver's runs use NCCL, one rank per GPU)
+    backend = os.environ.get("PS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     g, topo, md, desc = workload(args.config, args.ops)
@@ -204,7 +211,10 @@ def run_ours(args):
     first = rank * C
     init = initial_strategies(g, topo, md, first, C)
     from paper_1807_05358_b200.search import fit_capacity
-    low = lower(g, topo, prof, args.mode, max_degree=md, strategies=init, device=local)
+    # every rank lowers the same map set (the data-parallel start's maps first), so
+    # encoded strategies mean the same thing on every GPU for the final exchange
+    low = lower(g, topo, prof, args.mode, max_degree=md, strategies=[ps.data_parallel_strategy(g, topo)] + init,
+                device=local)
     L = nat.lib()
     maps = np.zeros((C, low.n_ops), dtype=np.int32)
     asg = np.zeros((C, low.n_slots), dtype=np.uint8)
