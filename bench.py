@@ -305,9 +305,17 @@ def run_ours(args):
 
     # ---- e2e: the C-ABI with host buffers, H2D of the step's inputs and D2H of its results inside the timing
     e2e_times = []
-    h2d = maps.nbytes + asg.nbytes + seeds.nbytes
-    best_maps = np.zeros((C, low.n_ops), dtype=np.int32)
-    best_asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+
+    def pinned(a):  # page-locked host copy (numpy view of pinned memory)
+        t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+        out = t.numpy()
+        out[...] = a
+        return out, t
+
+    (pmaps, _t1), (pasg, _t2), (pseeds, _t3) = pinned(maps), pinned(asg), pinned(seeds)
+    h2d = pmaps.nbytes + pasg.nbytes + pseeds.nbytes
+    best_maps, _t4 = pinned(np.zeros((C, low.n_ops), dtype=np.int32))
+    best_asg, _t5 = pinned(np.zeros((C, low.n_slots), dtype=np.uint8))
     d2h = ctypes.sizeof(nat.PsChainSummary) * C + best_maps.nbytes + best_asg.nbytes
     e2e_evals = 0
     for i in range(args.warmup + args.steps):
@@ -316,8 +324,8 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         h2 = ctypes.c_void_p()
-        nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
-                                   ctypes.byref(h2)), "ps_mcmc_create")
+        nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(pmaps), nat.ptr(pasg), nat.ptr(pseeds),
+                                   None, ctypes.byref(h2)), "ps_mcmc_create")
         run_step(h2)
         s2 = (nat.PsChainSummary * C)()
         nat.check(L.ps_mcmc_read(h2, s2, nat.ptr(best_maps), nat.ptr(best_asg), None, None), "ps_mcmc_read")
