@@ -345,3 +345,61 @@ def test_bench_config_mcmc_matches_oracle(oracle):
     assert got == want
     cand = np.array([c for _, c, _ in rep.trace]).reshape(C, P)
     assert np.array_equal(cand, ref["cand"])
+
+
+def _hetero_topology(rng):
+    """Two device kinds and three distinct link speeds: the multi-kind time table
+    and the per-transfer division path (more than two link classes)."""
+    topo = ps.DeviceTopology()
+    devs = []
+    for n in range(2):
+        for i in range(4):
+            kind = "gpu" if i < 2 else "tpu"
+            d = f"n{n}{kind}{i}"
+            topo.add_device(d, kind, f"node{n}")
+            devs.append((n, kind, d))
+    for x in range(len(devs)):
+        for y in range(x + 1, len(devs)):
+            (na, ka, a), (nb, kb, b) = devs[x], devs[y]
+            if na != nb:
+                bw, lat = 7e9, 5e-6
+            elif ka == kb == "tpu":
+                bw, lat = 32e9, 5e-7
+            else:
+                bw, lat = rng.choice(((16e9, 1e-6), (12e9, 2e-6)))
+            topo.add_connection(a, b, bw, lat)
+    return topo
+
+
+@pytest.mark.parametrize("shape", ["hetero8", "mesh64"])
+def test_randomised_sweep_matches_oracle(oracle, shape):
+    rng = random.Random(2026 if shape == "hetero8" else 2027)
+    for case in range(24):
+        g = ps.random_dag(rng.randint(10, 50), seed=rng.randrange(1 << 30))
+        if shape == "hetero8":
+            topo = _hetero_topology(rng)
+            prof = ps.CostProfile(fallback=ps.AnalyticCostModel(throughput={"tpu": 3e12}))
+        else:
+            topo = ps.multi_node_topology(16, 4)
+            prof = ps.CostProfile()
+        md = rng.choice((2, 4, 8))
+        strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, rng.randrange(1 << 20))
+                                                            for _ in range(3)]
+        for mode in (ps.MODE_FULL, ps.MODE_FORWARD):
+            got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=md)
+            want = oracle.makespans(g, topo, prof, mode, strategies)
+            assert list(got) == list(want), (shape, case, mode)
+
+
+def test_mcmc_on_heterogeneous_topology_matches_oracle(oracle):
+    rng = random.Random(99)
+    g = ps.random_dag(30, seed=1234)
+    topo = _hetero_topology(rng)
+    prof = ps.CostProfile(fallback=ps.AnalyticCostModel(throughput={"tpu": 3e12}))
+    init = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, 4, s) for s in range(3)]
+    for mode in (ps.MODE_FULL, ps.MODE_FORWARD):
+        rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=100, seed=11, max_degree=4, mode=mode,
+                                                            initial=init, polish=False, rng="philox"))
+        ref = oracle.mcmc(g, topo, prof, mode, init, [11 + 1000003 * c for c in range(4)], 100, 4, rng_mode="philox")
+        for ci, ch in enumerate(rep.chains):
+            assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted) == tuple(ref["summary"][ci][:4]), (mode, ci)
