@@ -1,22 +1,27 @@
 // parasim_cuda.cu -- B200 (sm_100a) strategy-evaluation path behind include/parasim.h.
 //
 // Kernels
-//   k_rows_count / k_rows_fill / k_cols_count / k_cols_fill
+//   k_rows / k_cols / k_pack
 //       Region-overlap tables: for every op pair and every (src degree map, dst
 //       degree map) combo, the (k, l, bytes) transfer list that _wire_pair
 //       derives for one strategy (reference taskgraph.py:154-195,
 //       partition.py:117-211), computed once per problem.  Rows (per src block
 //       k) are sorted by l; a column index (per dst block l) serves the
-//       backward pass.
-//   k_simulate_batch  one warp per candidate strategy: the task graph of the
-//       strategy is never materialised -- successors are walked straight out of
-//       the overlap tables -- and the reference's global (ready, origin) heap
-//       order (simulate.py:68-117) is reproduced exactly by a warp-wide argmin
-//       over a shared-memory ready set.  Per-queue (device / link) clocks live
-//       in shared memory.
+//       backward pass; k_pack writes 32-byte records with the other end's task
+//       slot and the transfer time per link class.
+//   k_simulate_batch  one warp per candidate strategy (candidates from a work
+//       queue): the task graph of the strategy is never materialised --
+//       successors are walked straight out of the overlap tables -- and the
+//       reference's global (ready, origin) heap order (simulate.py:68-117) is
+//       reproduced exactly by lookahead rounds over a shared-memory ready set
+//       (see "v2 simulator" below).  Per-queue (device / link) clocks live in
+//       shared memory.
 //   k_mcmc  persistent, one warp per chain: proposal (Philox4x32-10 or CPython
 //       MT19937 stream), in-place fragment rewrite, re-simulation, Metropolis
-//       accept, best snapshot, O(size) rollback (search.py:89-115,193-255).
+//       accept, best snapshot, O(size) rollback (search.py:89-115,193-255);
+//       time-boxed segments.
+//   k_simulate_trace  one strategy with every task and dependency recorded
+//       (the TaskGraph / timeline API); k_simulate_explicit  hand-built graphs.
 //
 // Exactness: the only floating-point operations on the simulated timeline are
 // max() and one IEEE add per task (start + exe), plus lat + bytes/bw for
