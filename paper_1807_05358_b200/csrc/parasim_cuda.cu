@@ -369,7 +369,7 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(4 * (size_t)P.n_pairs) * 2;              // prow, pcol
   b += asg_global ? 0 : al16((size_t)P.n_slots);     // asg
   b += al16(8 * (size_t)P.n_queues);                 // qclock (slow-path bids live in global scratch)
-  b += al16(8 * (size_t)P.cap) * 3 + al16(4 * (size_t)P.cap) * 2;  // ready set + member list
+  b += al16(32 * (size_t)P.cap) + al16(4 * (size_t)P.cap);  // ready set + member list
   b += al16(8 * (size_t)P.n_ops) + 16 + 128;         // per-op forward exe cache, flags, winner lanes
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC / 2);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
@@ -378,13 +378,15 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   return b;
 }
 
+struct __align__(16) REnt { unsigned long long h, k; double e; int q, pad; };
+
 struct W2 {
   int *mapl, *gmap, *fbase, *gbase, *prow, *pcol;
   unsigned char *asg;
   double *qclock;
-  unsigned long long *qready, *qbest, *rhi, *rlo;
-  double *rexe;
-  int *rq, *mem;
+  unsigned long long *qready, *qbest;
+  REnt *rs;  // ready set: (ready bits, origin key, exe, queue | flags), one 32-byte entry each
+  int *mem;
   double *exef;
   int *flags;  // [0]: slow-path queue bids may be dirty
   int *wlane;  // [32] lane holding the k-th winner of the round
@@ -465,10 +467,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.pcol = (int *)take(4 * P.n_pairs);
   w.asg = L.asg_global ? nullptr : (unsigned char *)take(P.n_slots);
   w.qclock = (double *)take(8 * P.n_queues);
-  w.rhi = (unsigned long long *)take(8 * P.cap);
-  w.rlo = (unsigned long long *)take(8 * P.cap);
-  w.rexe = (double *)take(8 * P.cap);
-  w.rq = (int *)take(4 * P.cap);
+  w.rs = (REnt *)take(sizeof(REnt) * P.cap);
   w.mem = (int *)take(4 * P.cap);
   w.exef = (double *)take(8 * P.n_ops);
   w.flags = (int *)take(16);
@@ -499,7 +498,7 @@ __host__ __device__ inline int overflow_cap(int n_slots) { return 4 * n_slots + 
 
 __host__ __device__ inline size_t gscratch_bytes(int n_slots, int n_queues) {
   return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 2) + al16((size_t)n_slots) +
-         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + (size_t)overflow_cap(n_slots) * 32 + 256;
+         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + (size_t)overflow_cap(n_slots) * 36 + 256;
 }
 
 // one warp's global slice: scratch, plus its whole shared-memory layout in global mode
@@ -534,11 +533,8 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
   char *g = gscratch + al16((size_t)P.n_slots * 3 * 8) + al16((size_t)P.n_slots * 3 * 2) + al16((size_t)P.n_slots) +
             al16((size_t)P.n_slots * 8) + al16((size_t)P.n_queues * 16);
   int c = overflow_cap(P.n_slots);
-  w.rhi = (unsigned long long *)g;
-  w.rlo = w.rhi + c;
-  w.rexe = (double *)(w.rlo + c);
-  w.rq = (int *)(w.rexe + c);
-  w.mem = w.rq + c;
+  w.rs = (REnt *)g;
+  w.mem = (int *)(w.rs + c);
   w.rcap = c;
   return w;
 }
@@ -575,10 +571,9 @@ __device__ __forceinline__ bool push2(bool want, double ready, unsigned long lon
   if (n + total > w.rcap) return false;
   if (want) {
     int pos = n + __popc(bm & ((1u << lane) - 1u));
-    w.rhi[pos] = (unsigned long long)__double_as_longlong(ready);
-    w.rlo[pos] = key;
-    w.rexe[pos] = exe;
-    w.rq[pos] = q;
+    REnt r;
+    r.h = (unsigned long long)__double_as_longlong(ready); r.k = key; r.e = exe; r.q = q; r.pad = 0;
+    w.rs[pos] = r;
   }
   n += total;
   return true;
@@ -912,10 +907,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     bool forced = false;
     if (n > 32 && n <= 64 && n + 32 <= w.rcap) {
       bool vA = true, vB = lane + 32 < n;
-      unsigned long long hA = w.rhi[lane], kA = w.rlo[lane], hB = vB ? w.rhi[lane + 32] : ~0ull,
-                         kB = vB ? w.rlo[lane + 32] : ~0ull;
-      double eA = w.rexe[lane], eB = vB ? w.rexe[lane + 32] : 0.0;
-      int qA = w.rq[lane], qB = vB ? w.rq[lane + 32] : 0;
+      unsigned long long hA = w.rs[lane].h, kA = w.rs[lane].k, hB = vB ? w.rs[lane + 32].h : ~0ull,
+                         kB = vB ? w.rs[lane + 32].k : ~0ull;
+      double eA = w.rs[lane].e, eB = vB ? w.rs[lane + 32].e : 0.0;
+      int qA = w.rs[lane].q, qB = vB ? w.rs[lane + 32].q : 0;
       double rA = __longlong_as_double((long long)hA), rB = __longlong_as_double((long long)hB);
       double cA = w.qclock[qA & Q_MASK], cB = vB ? w.qclock[qB & Q_MASK] : 0.0;
       double lA = (rA < cA ? cA : rA) + eA, lB = (rB < cB ? cB : rB) + eB;
@@ -931,8 +926,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int pA = mA ? 64 + __popc(gA & lt) : __popc(xA & lt);
         int pB = mB ? 64 + __popc(gA) + __popc(gB & lt) : __popc(xA) + __popc(xB & lt);
         __syncwarp();
-        w.rhi[pA] = hA; w.rlo[pA] = kA; w.rexe[pA] = eA; w.rq[pA] = qA;
-        if (vB) { w.rhi[pB] = hB; w.rlo[pB] = kB; w.rexe[pB] = eB; w.rq[pB] = qB; }
+        w.rs[pA].h = hA; w.rs[pA].k = kA; w.rs[pA].e = eA; w.rs[pA].q = qA;
+        if (vB) { w.rs[pB].h = hB; w.rs[pB].k = kB; w.rs[pB].e = eB; w.rs[pB].q = qB; }
         __syncwarp();
         sel_base = 64; sel_n = nm; rest = n - nm; forced = true;
       }
@@ -941,9 +936,12 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // ---- fast path: entry `lane` lives in this lane's registers for the round
       bool valid = lane < sel_n;
       int ix = sel_base + lane;
-      unsigned long long h = valid ? w.rhi[ix] : ~0ull, k = valid ? w.rlo[ix] : ~0ull;
-      double e = valid ? w.rexe[ix] : 0.0;
-      int qr = valid ? w.rq[ix] : 0;
+      REnt re;
+      re.h = ~0ull; re.k = ~0ull; re.e = 0.0; re.q = 0; re.pad = 0;
+      if (valid) re = w.rs[ix];
+      unsigned long long h = re.h, k = re.k;
+      double e = re.e;
+      int qr = re.q;
       int q = qr & Q_MASK;
       double r = __longlong_as_double((long long)h);
       // LB = min over tasks with successors of max(ready, clock) + exe: no task
@@ -990,7 +988,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       unsigned kb = __ballot_sync(FULLMASK, keep);
       if (keep) {
         int pos = __popc(kb & ((1u << lane) - 1u));
-        w.rhi[pos] = h; w.rlo[pos] = k; w.rexe[pos] = e; w.rq[pos] = qr;
+        REnt r2;
+        r2.h = h; r2.k = k; r2.e = e; r2.q = qr; r2.pad = 0;
+        w.rs[pos] = r2;
       }
       n = forced ? rest : __popc(kb);
       mine = win;
@@ -1012,12 +1012,12 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // ---- scan 1: minimum key and LB = min(ready + exe)
       unsigned long long bh = ~0ull, bl = ~0ull, lb = INF_BITS;
       for (int i = lane; i < n; i += 32) {
-        unsigned long long h = w.rhi[i], l = w.rlo[i];
+        unsigned long long h = w.rs[i].h, l = w.rs[i].k;
         if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; }
-        int qr = w.rq[i];
+        int qr = w.rs[i].q;
         if (!(qr & Q_SINK)) {
           double r0 = __longlong_as_double((long long)h), ck = w.qclock[qr & Q_MASK];
-          double e = (r0 < ck ? ck : r0) + w.rexe[i];
+          double e = (r0 < ck ? ck : r0) + w.rs[i].e;
           unsigned long long eb = (unsigned long long)__double_as_longlong(e);
           if (eb < lb) lb = eb;
         }
@@ -1032,9 +1032,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int i = base + lane;
         bool mem = false;
         if (i < n) {
-          unsigned long long h2 = w.rhi[i];
-          mem = __longlong_as_double((long long)h2) < LB || w.rlo[i] == minkey;
-          if (mem) atomicMin(&w.qready[w.rq[i] & Q_MASK], h2);
+          unsigned long long h2 = w.rs[i].h;
+          mem = __longlong_as_double((long long)h2) < LB || w.rs[i].k == minkey;
+          if (mem) atomicMin(&w.qready[w.rs[i].q & Q_MASK], h2);
         }
         unsigned bm = __ballot_sync(FULLMASK, mem);
         if (mem) w.mem[nm + __popc(bm & ((1u << lane) - 1u))] = i;
@@ -1044,8 +1044,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // ---- members tied on their queue's ready time bid their origin key
       for (int j = lane; j < nm; j += 32) {
         int i = w.mem[j];
-        int q2 = w.rq[i] & Q_MASK;
-        if (w.qready[q2] == w.rhi[i]) atomicMin(&w.qbest[q2], w.rlo[i]);
+        int q2 = w.rs[i].q & Q_MASK;
+        if (w.qready[q2] == w.rs[i].h) atomicMin(&w.qbest[q2], w.rs[i].k);
       }
       __syncwarp();
       // ---- winners: each queue's minimum (ready, origin); lane k holds winner k
@@ -1056,8 +1056,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int i = 0;
         if (j < nm) {
           i = w.mem[j];
-          int q2 = w.rq[i] & Q_MASK;
-          win = w.qbest[q2] == w.rlo[i] && w.qready[q2] == w.rhi[i];
+          int q2 = w.rs[i].q & Q_MASK;
+          win = w.qbest[q2] == w.rs[i].k && w.qready[q2] == w.rs[i].h;
         }
         unsigned bm = __ballot_sync(FULLMASK, win);
         // lane nw + r takes the r-th winner of this chunk (winners past 32 wait)
@@ -1069,18 +1069,18 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       bool mine0 = lane < nw;
       if (mine0) {
-        mykey = w.rlo[mypos];
-        myready = __longlong_as_double((long long)w.rhi[mypos]);
-        myexe = w.rexe[mypos];
-        myq = w.rq[mypos] & Q_MASK;
+        mykey = w.rs[mypos].k;
+        myready = __longlong_as_double((long long)w.rs[mypos].h);
+        myexe = w.rs[mypos].e;
+        myq = w.rs[mypos].q & Q_MASK;
       }
       __syncwarp();
-      if (mine0) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rhi[mypos] = ~0ull; }
+      if (mine0) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rs[mypos].h = ~0ull; }
       __syncwarp();
       // ---- remove the winners: refill holes below n-nw with survivors from the tail
       {
         int tailpos = n - nw + lane;
-        bool survivor = lane < nw && w.rhi[tailpos] != ~0ull;
+        bool survivor = lane < nw && w.rs[tailpos].h != ~0ull;
         unsigned sm = __ballot_sync(FULLMASK, survivor);
         bool head_hole = mine0 && mypos < n - nw;
         unsigned hm = __ballot_sync(FULLMASK, head_hole);
@@ -1090,9 +1090,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         unsigned long long h2 = 0, k2 = 0;
         double e2 = 0.0;
         int q2 = 0;
-        if (head_hole) { h2 = w.rhi[src]; k2 = w.rlo[src]; e2 = w.rexe[src]; q2 = w.rq[src]; }
+        if (head_hole) { h2 = w.rs[src].h; k2 = w.rs[src].k; e2 = w.rs[src].e; q2 = w.rs[src].q; }
         __syncwarp();
-        if (head_hole) { w.rhi[mypos] = h2; w.rlo[mypos] = k2; w.rexe[mypos] = e2; w.rq[mypos] = q2; }
+        if (head_hole) { w.rs[mypos].h = h2; w.rs[mypos].k = k2; w.rs[mypos].e = e2; w.rs[mypos].q = q2; }
         n -= nw;
         __syncwarp();
       }
