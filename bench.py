@@ -326,13 +326,20 @@ def run_ours(args):
         h2 = ctypes.c_void_p()
         nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(pmaps), nat.ptr(pasg), nat.ptr(pseeds),
                                    None, ctypes.byref(h2)), "ps_mcmc_create")
+        t1 = time.perf_counter()
         run_step(h2)
+        t2 = time.perf_counter()
         s2 = (nat.PsChainSummary * C)()
         nat.check(L.ps_mcmc_read(h2, s2, nat.ptr(best_maps), nat.ptr(best_asg), None, None), "ps_mcmc_read")
         dt = time.perf_counter() - t0
+        if os.environ.get("PS_BENCH_VERBOSE"):
+            print(f"e2e phases: create {1e3 * (t1 - t0):.2f} launch {1e3 * (t2 - t1):.2f} "
+                  f"read {1e3 * (time.perf_counter() - t2):.2f} ms", file=sys.stderr)
         L.ps_mcmc_destroy(h2)
         if i >= args.warmup:
             e2e_times.append(dt)
+            if os.environ.get("PS_BENCH_VERBOSE"):
+                print(f"e2e step {i}: {dt * 1e3:.2f} ms", file=sys.stderr)
             # evaluations = the initial scoring of every chain + its proposals
             e2e_evals += sum(s.proposals for s in s2) + C
     e2e_t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)

@@ -1767,6 +1767,16 @@ struct ps_problem {
   int *d_next = nullptr;  // batch work queue: next candidate to take
   char *mcmc_scratch = nullptr;  // chain scratch kept from the last destroyed MCMC handle
   size_t mcmc_scratch_bytes = 0;
+  // chain buffers kept from the last destroyed MCMC handle (create/run/destroy
+  // cycles, as in an end-to-end loop, then allocate nothing)
+  struct {
+    int n = 0;
+    int *maps = nullptr, *best_maps = nullptr;
+    unsigned char *asgs = nullptr, *best_asgs = nullptr;
+    void *st = nullptr;
+    double *d_best = nullptr;
+    int *d_bestc = nullptr;
+  } spare;
   size_t io_cap = 0;
   long long device_bytes = 0;
 };
@@ -1785,6 +1795,7 @@ struct ps_mcmc {
   size_t scratch_bytes = 0;
   double *d_best;
   int *d_bestc;
+  int cap_n;  // chains the buffers above were sized for
 };
 
 static int ensure_io(ps_problem *pr, size_t n) {
@@ -2018,6 +2029,8 @@ void ps_problem_destroy(ps_problem *pr) {
   cudaFree(pr->scratch);
   cudaFree(pr->d_map); cudaFree(pr->d_asg); cudaFree(pr->d_mk); cudaFree(pr->d_st); cudaFree(pr->d_next);
   cudaFree(pr->mcmc_scratch);
+  cudaFree(pr->spare.maps); cudaFree(pr->spare.best_maps); cudaFree(pr->spare.asgs); cudaFree(pr->spare.best_asgs);
+  cudaFree(pr->spare.st); cudaFree(pr->spare.d_best); cudaFree(pr->spare.d_bestc);
   delete pr;
 }
 
@@ -2224,11 +2237,21 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   m->n = n;
   m->params = *params;
   const DevProb &P = pr->P;
-  CK(cudaMalloc(&m->maps, (size_t)n * P.n_ops * sizeof(int)));
-  CK(cudaMalloc(&m->best_maps, (size_t)n * P.n_ops * sizeof(int)));
-  CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
-  CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
-  CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
+  if (pr->spare.maps && pr->spare.n >= n) {
+    m->maps = pr->spare.maps; m->best_maps = pr->spare.best_maps; m->asgs = pr->spare.asgs;
+    m->best_asgs = pr->spare.best_asgs; m->st = (ChainState *)pr->spare.st; m->d_best = pr->spare.d_best;
+    m->d_bestc = pr->spare.d_bestc; m->cap_n = pr->spare.n;
+    pr->spare.maps = nullptr; pr->spare.n = 0;
+  } else {
+    CK(cudaMalloc(&m->maps, (size_t)n * P.n_ops * sizeof(int)));
+    CK(cudaMalloc(&m->best_maps, (size_t)n * P.n_ops * sizeof(int)));
+    CK(cudaMalloc(&m->asgs, (size_t)n * P.n_slots));
+    CK(cudaMalloc(&m->best_asgs, (size_t)n * P.n_slots));
+    CK(cudaMalloc(&m->st, (size_t)n * sizeof(ChainState)));
+    CK(cudaMalloc(&m->d_best, sizeof(double)));
+    CK(cudaMalloc(&m->d_bestc, sizeof(int)));
+    m->cap_n = n;
+  }
   {
     size_t want = (size_t)n * gslice_bytes(P, pr->lay);
     if (pr->mcmc_scratch && pr->mcmc_scratch_bytes >= want) {  // reuse: repeated create/run/destroy cycles
@@ -2240,8 +2263,6 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
       m->scratch_bytes = want;
     }
   }
-  CK(cudaMalloc(&m->d_best, sizeof(double)));
-  CK(cudaMalloc(&m->d_bestc, sizeof(int)));
   CK(cudaMemcpy(m->maps, init_map, (size_t)n * P.n_ops * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(m->asgs, init_assign, (size_t)n * P.n_slots, cudaMemcpyHostToDevice));
   std::vector<ChainState> st(n);
@@ -2380,7 +2401,16 @@ int ps_mcmc_best(ps_mcmc *m, double *best_cost, int32_t *best_chain) {
 void ps_mcmc_destroy(ps_mcmc *m) {
   if (!m) return;
   cudaSetDevice(m->prob->device);
-  cudaFree(m->maps); cudaFree(m->best_maps); cudaFree(m->asgs); cudaFree(m->best_asgs); cudaFree(m->st);
+  ps_problem *pr = m->prob;
+  cudaDeviceSynchronize();  // kept buffers must be idle before a later handle reuses them (cudaFree would sync too)
+  if (!pr->spare.maps) {  // keep the chain buffers for the problem's next handle
+    pr->spare.n = m->cap_n; pr->spare.maps = m->maps; pr->spare.best_maps = m->best_maps; pr->spare.asgs = m->asgs;
+    pr->spare.best_asgs = m->best_asgs; pr->spare.st = m->st; pr->spare.d_best = m->d_best;
+    pr->spare.d_bestc = m->d_bestc;
+  } else {
+    cudaFree(m->maps); cudaFree(m->best_maps); cudaFree(m->asgs); cudaFree(m->best_asgs); cudaFree(m->st);
+    cudaFree(m->d_best); cudaFree(m->d_bestc);
+  }
   cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok);
   if (m->scratch) {  // keep the largest chain scratch for the problem's next handle
     if (m->scratch_bytes >= m->prob->mcmc_scratch_bytes) {
@@ -2391,7 +2421,6 @@ void ps_mcmc_destroy(ps_mcmc *m) {
       cudaFree(m->scratch);
     }
   }
-  cudaFree(m->d_best); cudaFree(m->d_bestc);
   delete m;
 }
 
