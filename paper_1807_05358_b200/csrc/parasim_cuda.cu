@@ -936,12 +936,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // ---- fast path: entry `lane` lives in this lane's registers for the round
       bool valid = lane < sel_n;
       int ix = sel_base + lane;
-      REnt re;
-      re.h = ~0ull; re.k = ~0ull; re.e = 0.0; re.q = 0; re.pad = 0;
-      if (valid) re = w.rs[ix];
-      unsigned long long h = re.h, k = re.k;
-      double e = re.e;
-      int qr = re.q;
+      REnt re = w.rs[valid ? ix : 0];  // unconditional load (entry 0 always exists), then mask
+      unsigned long long h = valid ? re.h : ~0ull, k = valid ? re.k : ~0ull;
+      double e = valid ? re.e : 0.0;
+      int qr = valid ? re.q : 0;
       int q = qr & Q_MASK;
       double r = __longlong_as_double((long long)h);
       // LB = min over tasks with successors of max(ready, clock) + exe: no task
