@@ -403,3 +403,43 @@ def test_mcmc_on_heterogeneous_topology_matches_oracle(oracle):
         ref = oracle.mcmc(g, topo, prof, mode, init, [11 + 1000003 * c for c in range(4)], 100, 4, rng_mode="philox")
         for ci, ch in enumerate(rep.chains):
             assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted) == tuple(ref["summary"][ci][:4]), (mode, ci)
+
+
+def test_time_boxed_segments_are_exact_prefixes(oracle):
+    """ps_mcmc_run_budget stops chains at data-dependent points (its time budget
+    and each chain's mean proposal time): whatever it stopped at, every chain's
+    state must equal the oracle's after that many proposals."""
+    import ctypes
+    from paper_1807_05358_b200 import _native as nat
+    from paper_1807_05358_b200.lowering import lower
+    g, topo, mode, md = _random_case(77)
+    prof = ps.CostProfile()
+    C = 48
+    init = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, c) for c in range(1, C)]
+    seeds = np.array([5 + 1000003 * c for c in range(C)], dtype=np.uint64)
+    low = lower(g, topo, prof, ps.MODE_FULL, max_degree=md, strategies=init)
+    maps = np.zeros((C, low.n_ops), dtype=np.int32)
+    asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+    for i, s in enumerate(init):
+        low.encode(s, maps[i], asg[i])
+    L = nat.lib()
+    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0)
+    h = ctypes.c_void_p()
+    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
+                               ctypes.byref(h)), "ps_mcmc_create")
+    try:
+        for _ in range(3):
+            nat.check(L.ps_mcmc_run_budget(h, 1 << 30, 300_000, None), "ps_mcmc_run_budget")  # 0.3 ms segments
+        summ = (nat.PsChainSummary * C)()
+        nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+    finally:
+        L.ps_mcmc_destroy(h)
+    counts = sorted({s.proposals for s in summ})
+    assert counts[-1] > 0
+    for p in counts:
+        idx = [c for c in range(C) if summ[c].proposals == p]
+        ref = oracle.mcmc(g, topo, prof, ps.MODE_FULL, [init[c] for c in idx], [int(seeds[c]) for c in idx], p, md,
+                          rng_mode="philox")
+        for j, c in enumerate(idx):
+            s = summ[c]
+            assert (s.initial_cost, s.best_cost, s.proposals, s.accepted) == tuple(ref["summary"][j][:4]), (c, p)
