@@ -1158,9 +1158,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int wdev = 0, L = 0;
     int fe = -1, fp = 0;  // this lane's first list entry (index j0) and its pair
     // fixed successor: fact 1 = arrive at counter fslot, 2 = push task fkey directly
-    int fact = 0, fslot = 0, fq = 0, fea = -1, feb = -1;
-    unsigned long long fkey = 0;
-    double fexe = 0.0;
+    // (the f* values are only read where fact != 0: left uninitialised, no moves)
+    int fact = 0, fslot, fq, fea = -1, feb = -1;
+    unsigned long long fkey;
+    double fexe;
     bool ferr = false;
     if (act_lane) {
       if (fwd || kind == KIND_OP_BWD) {
@@ -1216,7 +1217,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
     }
     Ent32 fen;
-    fen.kl = 0; fen.slot = 0; fen.bytes = 0; fen.exe[0] = fen.exe[1] = 0.0;
+    // (read only by lanes with an entry: fe >= 0 whenever j0 < L)
     TC(11);
     if (fe >= 0) fen = etab[fe];
     int Lt = L + (fact ? 1 : 0);
@@ -1229,10 +1230,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     for (int t = 0; t < iters; ++t) {
       int idx = j0 + t * G;
       int act = 0;  // 1 arrive at counter `slot`, 2 push task `skey` directly
-      int slot = 0;
-      unsigned long long skey = 0;
-      int pq = 0;
-      double pexe = 0.0;
+      int slot;               // read only when act == 1
+      unsigned long long skey;  // stored only for lanes that push
+      int pq;
+      double pexe;
       bool err = false;
       int ea = -1, eb = -1;
       if (act_lane && idx < L) {
