@@ -894,11 +894,12 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     PH_CNT(12, n);
     bool mine = false;
     int nw = 0;
-    unsigned long long mykey = 0;
-    double myready = 0.0, myexe = 0.0;
-    int myq = -1;
+    // (the winner's task: read only on winner lanes, or shuffled from them)
+    unsigned long long mykey;
+    double myready, myexe;
+    int myq;
     int myrank = 0, maxrank = 0;  // position among this round's members on the same queue
-    double end = 0.0, mystart = 0.0;
+    double end, mystart;  // set on winner lanes
     bool ran = false;  // fast path: rank-0 members already ran (their queue clock is the one read this round)
     // Medium path (33..64 ready tasks, two per lane): when the round's members
     // are at most 32, they are staged at [64, 64 + members) and the others
