@@ -542,7 +542,7 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
 // simulator variants: SIM_TRACE records every task and dependency
 // (k_simulate_trace), SIM_OPMIN keeps each op's earliest forward end (exhaustive
 // search bounds); the MCMC kernel compiles neither
-enum { SIM_TRACE = 1, SIM_OPMIN = 2 };
+enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4 };
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
 
@@ -704,11 +704,13 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
 }
 
 // exe time / queue of a transfer between devices da -> db carrying nb bytes
+// simple: the problem has one device kind and <= 2 link classes (a compile-time
+// constant in the evaluation kernels' common variant, which drops the other paths)
 __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int da, int db, double nb, int &q,
-                                           double &exe) {
+                                           double &exe, bool simple = false) {
   int lv = T.link_of[da * P.n_dev + db];
   if (lv < 0) return false;
-  if (P.n_cls) {
+  if (simple || P.n_cls) {
     q = P.n_dev + (lv & 0x3fff);
     exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + nb / ((lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
   } else {
@@ -719,15 +721,15 @@ __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int d
 }
 
 __device__ __forceinline__ void op_attrs(const DevProb &P, const Tab &T, const W2 &w, unsigned kind, int a, int c,
-                                         int &q, double &exe) {
+                                         int &q, double &exe, bool simple = false) {
   int dev = w.asg[T.op_slot_off[a] + c];
   q = dev;
-  if (P.n_kinds == 1) exe = kind == KIND_OP ? w.exef[a] : __dmul_rn(w.exef[a], P.mult);
+  if (simple || P.n_kinds == 1) exe = kind == KIND_OP ? w.exef[a] : __dmul_rn(w.exef[a], P.mult);
   else exe = (kind == KIND_OP ? P.exe_fwd : P.exe_bwd)[w.gmap[a] * P.n_kinds + T.dev_kind[dev]];
 }
 
 __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const W2 &w, const State &st, int a, int si,
-                                           int hop, int &q, double &exe, int &ea, int &eb) {
+                                           int hop, int &q, double &exe, int &ea, int &eb, bool simple = false) {
   int gi = w.gbase[a] + si;
   unsigned long long msk = st.gmask[gi];
   int r = __popcll((long long)msk);
@@ -739,15 +741,15 @@ __device__ __forceinline__ bool sync_attrs(const DevProb &P, const Tab &T, const
   double nb;
   if (hop == 0) { nb = P.map_shard[w.gmap[a]] / (double)r; *per = nb; }
   else nb = *per;
-  if (!link_attrs(P, T, da, db, nb, q, exe)) { ea = da; eb = db; return false; }
+  if (!link_attrs(P, T, da, db, nb, q, exe, simple)) { ea = da; eb = db; return false; }
   if (hop + 1 >= 2 * (r - 1)) q |= Q_SINK;
   return true;
 }
 
 // queue / time of the transfer an overlap record creates between da -> db
 __device__ __forceinline__ bool link_attrs_ent(const DevProb &P, const Tab &T, int da, int db, const Ent32 &en,
-                                               int &q, double &exe) {
-  if (!P.n_cls) return link_attrs(P, T, da, db, (double)en.bytes, q, exe);
+                                               int &q, double &exe, bool simple = false) {
+  if (!simple && !P.n_cls) return link_attrs(P, T, da, db, (double)en.bytes, q, exe);
   int lv = T.link_of[da * P.n_dev + db];
   if (lv < 0) return false;
   q = P.n_dev + (lv & 0x3fff);
@@ -797,6 +799,7 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
 
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
+  constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes
   SimOut out;
   out.makespan = 0.0;
   out.status = PS_STATUS_OK;
@@ -879,7 +882,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     if (s < Tf && st.rem[s] == 0) {
       int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
       key = pack_key(KIND_OP, o, 0, s - w.fbase[o], 0);
-      op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe);
+      op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe, SIMPLE);
       want = true;
     }
     okc &= push2(want, 0.0, key, exe, q, n, P, w, lane);
@@ -1213,7 +1216,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         int r = __popcll((long long)st.gmask[w.gbase[a] + b]);
         if ((int)c + 1 < 2 * (r - 1)) {
           fact = 2; fkey = pack_key(KIND_SYNC, a, b, c + 1, 0);
-          if (!sync_attrs(P, T, w, st, a, b, c + 1, fq, fexe, fea, feb)) ferr = true;
+          if (!sync_attrs(P, T, w, st, a, b, c + 1, fq, fexe, fea, feb, SIMPLE)) ferr = true;
         }
       }
     }
@@ -1265,7 +1268,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           int so = fwd ? (int)a : xo, dop = fwd ? xo : (int)a, sb = fwd ? (int)c : kk, db = fwd ? l : (int)c;
           int sdv = fwd ? wdev : xdev, ddv = fwd ? xdev : wdev;
           skey = pack_key(fwd ? KIND_EDGE : KIND_EDGE_BWD, so, dop, sb, db);
-          if (!link_attrs_ent(P, T, sdv, ddv, en, pq, pexe)) { err = true; ea = sdv; eb = ddv; }
+          if (!link_attrs_ent(P, T, sdv, ddv, en, pq, pexe, SIMPLE)) { err = true; ea = sdv; eb = ddv; }
         }
       } else if (act_lane && idx == L && fact) {
         act = fact; slot = fslot; skey = fkey; pq = fq; pexe = fexe; err = ferr; ea = fea; eb = feb;
@@ -1306,9 +1309,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           pready = cur;
           unsigned sk = key_kind(skey);
           if (sk == KIND_SYNC) {
-            if (!sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb)) err = true;
+            if (!sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb, SIMPLE)) err = true;
           } else {
-            op_attrs(P, T, w, sk, key_a(skey), key_c(skey), pq, pexe);
+            op_attrs(P, T, w, sk, key_a(skey), key_c(skey), pq, pexe, SIMPLE);
           }
         }
       } else if (act == 2) {
@@ -1342,6 +1345,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   return out;
 }
 
+template <int S>
 __global__ void __launch_bounds__(256, 1)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
                  double *makespan, int *status, char *gscratch, double *opmin, int *next) {
@@ -1371,7 +1375,7 @@ k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigne
       for (int i = lane; i < P.n_ops; i += 32) w.opmin[i] = __longlong_as_double(0x7ff0000000000000ll);
     }
     __syncwarp();
-    SimOut o = opmin ? simulate_any<SIM_OPMIN>(P, T, w, lay, gs, lane) : simulate_any<0>(P, T, w, lay, gs, lane);
+    SimOut o = opmin ? simulate_any<SIM_OPMIN | S>(P, T, w, lay, gs, lane) : simulate_any<S>(P, T, w, lay, gs, lane);
     if (lane == 0) {
       makespan[cand] = o.status == PS_STATUS_OK ? o.makespan : -1.0;
       status[cand] = o.status;
@@ -1562,6 +1566,7 @@ struct WarpRng {
   }
 };
 
+template <int S>
 __global__ void __launch_bounds__(256, 1)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
@@ -1646,7 +1651,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     if (same) {
       cand = cs.cost;
     } else {
-      SimOut so = simulate_any<0>(P, T, w, lay, gs, lane);
+      SimOut so = simulate_any<S>(P, T, w, lay, gs, lane);
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
         if (it < 0) {
@@ -2006,11 +2011,13 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   }
   // the attribute is per kernel, not per problem: allow the device maximum so
   // problems with different layouts can coexist
-  CK(cudaFuncSetAttribute(k_simulate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_simulate_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_simulate_batch<SIM_SIMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch, pr->wpb * 32, pr->smem_per_block));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch<0>, pr->wpb * 32, pr->smem_per_block));
   if (getenv("PS_DEBUG"))
     fprintf(stderr, "[parasim] tab=%zu warp=%zu SC=%d GC=%d RC=%d wpb=%d smem/block=%zu occ=%d optin=%d per_sm=%d\n",
             pr->lay.tab_bytes, pr->lay.warp_bytes, pr->lay.SC, pr->lay.GC, pr->lay.RC, pr->wpb, pr->smem_per_block, occ,
@@ -2111,7 +2118,8 @@ int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t
   }
   if (!pr->d_next) CK(cudaMalloc(&pr->d_next, sizeof(int)));
   CK(cudaMemsetAsync(pr->d_next, 0, sizeof(int), s));
-  k_simulate_batch<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop,
+  auto kb = (pr->P.n_kinds == 1 && pr->P.n_cls > 0) ? k_simulate_batch<SIM_SIMPLE> : k_simulate_batch<0>;
+  kb<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop,
                                                                  pr->d_next);
   CK(cudaGetLastError());
   if (flags != PS_DEVICE_PTRS) {
@@ -2297,7 +2305,8 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   int wpb = pr->wpb;
   int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
-  k_mcmc<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
+  auto km = (pr->P.n_kinds == 1 && pr->P.n_cls > 0) ? k_mcmc<SIM_SIMPLE> : k_mcmc<0>;
+  km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
       m->params.record_trace ? m->params.trace_capacity : 0, m->scratch, budget_ns);
