@@ -704,12 +704,13 @@ __device__ inline State setup_candidate(const DevProb &P, const Tab &T, const W2
 }
 
 // exe time / queue of a transfer between devices da -> db carrying nb bytes
-// simple: the problem has one device kind and <= 2 link classes (a compile-time
-// constant in the evaluation kernels' common variant, which drops the other paths)
+// simple: the problem has one device kind, <= 2 link classes and a link between
+// every pair of devices (a compile-time constant in the evaluation kernels'
+// common variant, which drops the other paths and the missing-route checks)
 __device__ __forceinline__ bool link_attrs(const DevProb &P, const Tab &T, int da, int db, double nb, int &q,
                                            double &exe, bool simple = false) {
   int lv = T.link_of[da * P.n_dev + db];
-  if (lv < 0) return false;
+  if (!simple && lv < 0) return false;
   if (simple || P.n_cls) {
     q = P.n_dev + (lv & 0x3fff);
     exe = ((lv >> 14) ? P.cls_lat[1] : P.cls_lat[0]) + nb / ((lv >> 14) ? P.cls_bw[1] : P.cls_bw[0]);
@@ -751,7 +752,7 @@ __device__ __forceinline__ bool link_attrs_ent(const DevProb &P, const Tab &T, i
                                                int &q, double &exe, bool simple = false) {
   if (!simple && !P.n_cls) return link_attrs(P, T, da, db, (double)en.bytes, q, exe);
   int lv = T.link_of[da * P.n_dev + db];
-  if (lv < 0) return false;
+  if (!simple && lv < 0) return false;
   q = P.n_dev + (lv & 0x3fff);
   exe = (lv >> 14) ? en.exe[1] : en.exe[0];
   return true;
@@ -799,7 +800,7 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
 
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
-  constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes
+  constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
   SimOut out;
   out.makespan = 0.0;
   out.status = PS_STATUS_OK;
@@ -1319,13 +1320,15 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         pready = wend;
       }
       if (t == 0) TC(14);
-      unsigned bad = __ballot_sync(FULLMASK, err);
-      if (bad) {
-        int s3 = __ffs(bad) - 1;
-        out.status = PS_STATUS_NO_ROUTE;
-        out.err_a = __shfl_sync(FULLMASK, ea, s3);
-        out.err_b = __shfl_sync(FULLMASK, eb, s3);
-        return out;
+      if (!SIMPLE) {  // (a full mesh has a route for every transfer)
+        unsigned bad = __ballot_sync(FULLMASK, err);
+        if (bad) {
+          int s3 = __ffs(bad) - 1;
+          out.status = PS_STATUS_NO_ROUTE;
+          out.err_a = __shfl_sync(FULLMASK, ea, s3);
+          out.err_b = __shfl_sync(FULLMASK, eb, s3);
+          return out;
+        }
       }
       if (!push2(want, pready, skey, pexe, pq, n, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
       __syncwarp();
@@ -1770,6 +1773,7 @@ struct ps_problem {
   double *d_mk = nullptr;
   int *d_st = nullptr;
   int *d_next = nullptr;  // batch work queue: next candidate to take
+  bool simple = false;    // kernels' SIM_SIMPLE variant applies (one kind, <= 2 link classes, full mesh)
   char *mcmc_scratch = nullptr;  // chain scratch kept from the last destroyed MCMC handle
   size_t mcmc_scratch_bytes = 0;
   // chain buffers kept from the last destroyed MCMC handle (create/run/destroy
@@ -1889,6 +1893,11 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
       cls[li] = c;
     }
     P.n_cls = (ncls <= 2 && P.n_links < 16384) ? ncls : 0;
+    bool mesh = true;
+    for (int i = 0; i < P.n_dev && mesh; ++i)
+      for (int j = 0; j < P.n_dev; ++j)
+        if (i != j && d->link_of[i * P.n_dev + j] < 0) { mesh = false; break; }
+    pr->simple = mesh && P.n_cls > 0 && P.n_kinds == 1;
     std::vector<short> l16((size_t)P.n_dev * P.n_dev);
     for (size_t i = 0; i < l16.size(); ++i) {
       int li = d->link_of[i];
@@ -2118,7 +2127,7 @@ int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t
   }
   if (!pr->d_next) CK(cudaMalloc(&pr->d_next, sizeof(int)));
   CK(cudaMemsetAsync(pr->d_next, 0, sizeof(int), s));
-  auto kb = (pr->P.n_kinds == 1 && pr->P.n_cls > 0) ? k_simulate_batch<SIM_SIMPLE> : k_simulate_batch<0>;
+  auto kb = pr->simple ? k_simulate_batch<SIM_SIMPLE> : k_simulate_batch<0>;
   kb<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop,
                                                                  pr->d_next);
   CK(cudaGetLastError());
@@ -2305,7 +2314,7 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   int wpb = pr->wpb;
   int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
-  auto km = (pr->P.n_kinds == 1 && pr->P.n_cls > 0) ? k_mcmc<SIM_SIMPLE> : k_mcmc<0>;
+  auto km = pr->simple ? k_mcmc<SIM_SIMPLE> : k_mcmc<0>;
   km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
