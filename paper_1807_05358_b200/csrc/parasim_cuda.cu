@@ -542,7 +542,7 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
 // simulator variants: SIM_TRACE records every task and dependency
 // (k_simulate_trace), SIM_OPMIN keeps each op's earliest forward end (exhaustive
 // search bounds); the MCMC kernel compiles neither
-enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4 };
+enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4, SIM_FULL = 8, SIM_FWD = 16 };
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
 
@@ -801,6 +801,10 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
+  // mode known at compile time in the specialised variants (forward mode then
+  // drops every backward / ring path)
+  constexpr int MODE = (M & SIM_FULL) ? 1 : (M & SIM_FWD) ? 0 : -1;
+  const bool FULL = MODE == 1 ? true : MODE == 0 ? false : (P.full != 0);
   SimOut out;
   out.makespan = 0.0;
   out.status = PS_STATUS_OK;
@@ -816,7 +820,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   PH_CNT(8, 1);
   PH_CNT(9, st.rowoff == w.srow ? 1 : 0);
   const int Tf = st.Tf;
-  PH_CNT(10, (P.full ? 2 * Tf + st.G : Tf) <= L.SC ? 1 : 0);
+  PH_CNT(10, (FULL ? 2 * Tf + st.G : Tf) <= L.SC ? 1 : 0);
   const Ent32 *ent = (const Ent32 *)P.ent16;
   const Ent32 *cent = (const Ent32 *)P.cent16;
   const bool was_dirty = w.flags[0] != 0;
@@ -827,7 +831,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   __syncwarp();
   if (lane == 0) w.flags[0] = 0;
   bool dirty = false;  // register copy of w.flags[0] for this simulation
-  if (P.full)
+  if (FULL)
     for (int s = lane; s < st.G; s += 32) st.gmask[s] = 0ull;
   __syncwarp();
   // ---- init: in-degrees, ring membership
@@ -838,7 +842,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int indeg = 0;
     for (int i = T.op_in_off[o]; i < T.op_in_off[o + 1]; ++i) {
       int col = w.pcol[T.op_in_pairs[i]] + k;
-      if (P.full) indeg += st.coloff[col + 1] - st.coloff[col];
+      if (FULL) indeg += st.coloff[col + 1] - st.coloff[col];
       else {  // forward mode: columns are not staged; count from the global index
         int p = T.op_in_pairs[i];
         int sp = T.pair_src[p];
@@ -849,7 +853,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     }
     st.rem[s] = (unsigned short)indeg;
     st.ready[s] = 0.0;
-    if (P.full) {
+    if (FULL) {
       int outd = 1;
       for (int i = T.op_out_off[o]; i < T.op_out_off[o + 1]; ++i) {
         int row = w.prow[T.op_out_pairs[i]] + k;
@@ -1153,6 +1157,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int wrec = __shfl_sync(FULLMASK, myrec, srcl);
     int wq = __shfl_sync(FULLMASK, myq, srcl);  // an operator task's queue is its device
     unsigned kind = key_kind(wkey), a = key_a(wkey), b = key_b(wkey), c = key_c(wkey), d = key_d(wkey);
+    if (MODE == 0) kind = kind == KIND_OP ? KIND_OP : KIND_EDGE;  // forward mode: no other kinds
     const bool fwd = kind == KIND_OP;
     TC(10);
     const int *poff = fwd ? T.op_out_off : T.op_in_off;
@@ -1206,7 +1211,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           }
         }
       }
-      if ((fwd && P.full) || kind == KIND_EDGE || kind == KIND_EDGE_BWD) {
+      if ((fwd && FULL) || kind == KIND_EDGE || kind == KIND_EDGE_BWD) {
         // forward -> its backward task; transfer -> the task it feeds
         bool tf = kind == KIND_EDGE;
         int xo = tf ? (int)b : (int)a, xb = tf ? (int)d : (int)c;
@@ -1308,7 +1313,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         if (last) {
           want = true;
           pready = cur;
-          unsigned sk = key_kind(skey);
+          unsigned sk = MODE == 0 ? (unsigned)KIND_OP : key_kind(skey);  // forward: arrivals feed forward ops
           if (sk == KIND_SYNC) {
             if (!sync_attrs(P, T, w, st, key_a(skey), key_b(skey), 0, pq, pexe, ea, eb, SIMPLE)) err = true;
           } else {
@@ -2021,9 +2026,11 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   // the attribute is per kernel, not per problem: allow the device maximum so
   // problems with different layouts can coexist
   CK(cudaFuncSetAttribute(k_simulate_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_simulate_batch<SIM_SIMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_simulate_batch<SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_simulate_batch<SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_mcmc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch<0>, pr->wpb * 32, pr->smem_per_block));
@@ -2127,7 +2134,8 @@ int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t
   }
   if (!pr->d_next) CK(cudaMalloc(&pr->d_next, sizeof(int)));
   CK(cudaMemsetAsync(pr->d_next, 0, sizeof(int), s));
-  auto kb = pr->simple ? k_simulate_batch<SIM_SIMPLE> : k_simulate_batch<0>;
+  auto kb = !pr->simple ? k_simulate_batch<0>
+            : pr->P.full ? k_simulate_batch<SIM_SIMPLE | SIM_FULL> : k_simulate_batch<SIM_SIMPLE | SIM_FWD>;
   kb<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop,
                                                                  pr->d_next);
   CK(cudaGetLastError());
@@ -2314,7 +2322,7 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   int wpb = pr->wpb;
   int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
-  auto km = pr->simple ? k_mcmc<SIM_SIMPLE> : k_mcmc<0>;
+  auto km = !pr->simple ? k_mcmc<0> : pr->P.full ? k_mcmc<SIM_SIMPLE | SIM_FULL> : k_mcmc<SIM_SIMPLE | SIM_FWD>;
   km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
