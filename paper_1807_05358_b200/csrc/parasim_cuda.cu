@@ -1343,7 +1343,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 #ifdef PS_TCYC
     ++tc_r;
 #endif
-    __syncwarp();
+    // (no barrier here: every path above ends with one after its last shared store)
   }
   // makespan: max over lanes
   unsigned long long mb = (unsigned long long)__double_as_longlong(out.makespan);
