@@ -165,7 +165,7 @@ typedef struct ps_mcmc_params {
   double beta;
   double ln10;            /* math.log(10.0) of the host */
   int32_t record_trace;   /* keep (cand, accepted) per proposal */
-  int32_t trace_capacity; /* proposals recorded per chain */
+  int32_t trace_capacity; /* ring of proposals recorded per chain: proposal i lands in slot i % capacity */
 } ps_mcmc_params;
 
 typedef struct ps_chain_summary {

@@ -1688,9 +1688,12 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
       double pr = exp(__dmul_rn(cs.beta, __dsub_rn(cs.cost, cand)));
       ok = pr >= 1.0 ? true : rng.random() < pr;
     }
-    if (trace_cap > 0 && idx < trace_cap && lane == 0) {
-      trace_cand[(size_t)chain * trace_cap + idx] = cand;
-      trace_ok[(size_t)chain * trace_cap + idx] = ok;
+    if (trace_cap > 0 && lane == 0) {
+      // a ring of trace_cap proposals per chain: the host reads it back at least
+      // every trace_cap proposals (time-boxed searches read it after each segment)
+      size_t slot = (size_t)chain * trace_cap + (size_t)(idx % trace_cap);
+      trace_cand[slot] = cand;
+      trace_ok[slot] = ok;
     }
     if (cand < cs.best) {
       cs.best = cand;
@@ -1828,6 +1831,15 @@ extern "C" {
 const char *ps_last_error(void) { return g_err.c_str(); }
 int ps_abi_version(void) { return PS_ABI_VERSION; }
 
+namespace {
+// frees temporary device buffers on every exit path of problem_build
+struct TmpBufs {
+  std::vector<void *> p;
+  ~TmpBufs() { for (void *x : p) cudaFree(x); }
+};
+int problem_build(const ps_problem_desc *d, int device, ps_problem *pr);
+}  // namespace
+
 int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   if (!d || !out) return fail(PS_ERR_INVALID, "null argument");
   if (d->abi_version != PS_ABI_VERSION) return fail(PS_ERR_INVALID, "ABI version mismatch");
@@ -1836,6 +1848,21 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   CK(cudaSetDevice(device));
   ps_problem *pr = new ps_problem();
   pr->device = device;
+  int rc = problem_build(d, device, pr);
+  if (rc != PS_OK) {
+    std::string msg = g_err;
+    ps_problem_destroy(pr);  // every buffer allocated so far is owned by pr
+    g_err = msg;
+    return rc;
+  }
+  *out = pr;
+  return PS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
   DevProb &P = pr->P;
   P.n_ops = d->n_ops; P.n_dev = d->n_devices; P.n_kinds = d->n_kinds; P.n_links = d->n_links;
   P.n_pairs = d->n_pairs; P.n_maps = d->n_maps; P.full = d->mode_full; P.n_slots = d->n_slots;
@@ -1849,15 +1876,13 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   int n_need = d->pair_need_off[d->n_pairs];
   int rc = PS_OK;
 #define UP(field, count) \
-  if ((rc = upload(ow, d->field, (size_t)(count), &P.field)) != PS_OK) { ps_problem_destroy(pr); return rc; }
+  if ((rc = upload(ow, d->field, (size_t)(count), &P.field)) != PS_OK) return rc;
   UP(dev_kind, P.n_dev);
   UP(link_of, (size_t)P.n_dev * P.n_dev);
   UP(link_bw, P.n_links);
   UP(link_lat, P.n_links);
   UP(op_ndim, P.n_ops);
-  if ((rc = upload(ow, (const long long *)d->op_dim, (size_t)P.n_ops * PS_MAXDIM, &P.op_dim)) != PS_OK) {
-    ps_problem_destroy(pr); return rc;
-  }
+  if ((rc = upload(ow, (const long long *)d->op_dim, (size_t)P.n_ops * PS_MAXDIM, &P.op_dim)) != PS_OK) return rc;
   UP(op_esize, P.n_ops);
   UP(op_param_mask, P.n_ops);
   UP(op_map_off, P.n_ops + 1);
@@ -1908,17 +1933,21 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
       int li = d->link_of[i];
       l16[i] = (short)(li < 0 ? -1 : (P.n_cls ? (li | cls[li] << 14) : li));
     }
-    if ((rc = upload(ow, l16.data(), l16.size(), &P.link16)) != PS_OK) { ps_problem_destroy(pr); return rc; }
+    if ((rc = upload(ow, l16.data(), l16.size(), &P.link16)) != PS_OK) return rc;
   }
   // ---- overlap tables: count rows -> scan -> fill, then the column index
   int *cnt = nullptr, *off = nullptr, *ccnt = nullptr, *coff = nullptr;
   void *tmp = nullptr;
   size_t tmp_bytes = 0, t2 = 0;
+  TmpBufs tb_;
   CK(cudaMalloc(&cnt, (n_rows + 1) * sizeof(int)));
+  tb_.p.push_back(cnt);
   CK(cudaMalloc(&off, (n_rows + 1) * sizeof(int)));
+  ow.push_back(off);
   CK(cudaMalloc(&ccnt, (n_cols + 1) * sizeof(int)));
+  tb_.p.push_back(ccnt);
   CK(cudaMalloc(&coff, (n_cols + 1) * sizeof(int)));
-  ow.push_back(off); ow.push_back(coff);
+  ow.push_back(coff);
   CK(cudaMemset(cnt, 0, (n_rows + 1) * sizeof(int)));
   CK(cudaMemset(ccnt, 0, (n_cols + 1) * sizeof(int)));
   if (n_rows) k_rows<<<(n_rows + 127) / 128, 128>>>(P, n_rows, n_combos, cnt, nullptr);
@@ -1927,6 +1956,7 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   cub::DeviceScan::ExclusiveSum(nullptr, t2, ccnt, coff, n_cols + 1);
   tmp_bytes = std::max(tmp_bytes, t2);
   CK(cudaMalloc(&tmp, tmp_bytes));
+  tb_.p.push_back(tmp);
   CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, n_rows + 1));
   int n_ent = 0;
   CK(cudaMemcpy(&n_ent, off + n_rows, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1935,10 +1965,13 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   long long *eb = nullptr;
   int *cent = nullptr;
   CK(cudaMalloc(&ek, (n_ent + 1) * sizeof(unsigned short)));
+  ow.push_back(ek);
   CK(cudaMalloc(&el, (n_ent + 1) * sizeof(unsigned short)));
+  ow.push_back(el);
   CK(cudaMalloc(&eb, (n_ent + 1) * sizeof(long long)));
+  ow.push_back(eb);
   CK(cudaMalloc(&cent, (n_ent + 1) * sizeof(int)));
-  ow.push_back(ek); ow.push_back(el); ow.push_back(eb); ow.push_back(cent);
+  ow.push_back(cent);
   P.ent_k = ek; P.ent_l = el; P.ent_bytes = eb; P.col_ent = cent; P.row_ent_off = off;
   if (n_rows) k_rows<<<(n_rows + 127) / 128, 128>>>(P, n_rows, n_combos, nullptr, off);
   CK(cudaGetLastError());
@@ -1950,13 +1983,13 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
   CK(cudaGetLastError());
   void *e16 = nullptr, *c16 = nullptr;
   CK(cudaMalloc(&e16, (size_t)(n_ent + 1) * sizeof(Ent32)));
+  ow.push_back(e16);
   CK(cudaMalloc(&c16, (size_t)(n_ent + 1) * sizeof(Ent32)));
-  ow.push_back(e16); ow.push_back(c16);
+  ow.push_back(c16);
   P.ent16 = e16; P.cent16 = c16;
   if (n_ent) k_pack<<<(n_ent + 127) / 128, 128>>>(P, n_ent, (int)n_rows, (int)n_combos, e16, c16);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
-  cudaFree(cnt); cudaFree(ccnt); cudaFree(tmp);
   // ---- launch geometry: largest shared-state capacity S that still keeps
   // >= 8 resident warps (candidates) per SM; warps per block in {4, 2, 1}
   CK(cudaDeviceGetAttribute(&pr->sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -2038,12 +2071,14 @@ int ps_problem_create(const ps_problem_desc *d, int device, ps_problem **out) {
     fprintf(stderr, "[parasim] tab=%zu warp=%zu SC=%d GC=%d RC=%d wpb=%d smem/block=%zu occ=%d optin=%d per_sm=%d\n",
             pr->lay.tab_bytes, pr->lay.warp_bytes, pr->lay.SC, pr->lay.GC, pr->lay.RC, pr->wpb, pr->smem_per_block, occ,
             optin, per_sm);
-  if (occ < 1) { ps_problem_destroy(pr); return fail(PS_ERR_CAPACITY, "kernel does not fit on an SM"); }
+  if (occ < 1) return fail(PS_ERR_CAPACITY, "kernel does not fit on an SM");
   pr->blocks_per_sm = occ;
   pr->device_bytes = 0;
-  *out = pr;
   return PS_OK;
 }
+}  // namespace
+
+extern "C" {
 
 void ps_problem_destroy(ps_problem *pr) {
   if (!pr) return;

@@ -306,6 +306,11 @@ def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree
             region0 = output_region(op, cfg, 0)
             for kname, ki in kind_index.items():
                 e = profile.task_exe_time(op, region0, dev_of_kind[kname])
+                if not e >= 0.0:
+                    # the reference would schedule a negative (or NaN) time; its heap order
+                    # is then no longer monotone in ready time, which the GPU replay assumes
+                    raise ValueError(f"op {oid}: task time {e!r} for {kname} is negative or NaN; "
+                                     "the GPU path needs non-negative task times")
                 exe_fwd[gi, ki] = e
                 exe_bwd[gi, ki] = e * mult
             if op_param_mask[r] >= 0:

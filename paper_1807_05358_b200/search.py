@@ -144,8 +144,9 @@ def evaluate_strategies(g: OperatorGraph, topo: DeviceTopology, profile: CostPro
     return _eval_encoded(low, maps, asg, strategies)
 
 
-def _eval_encoded(low, maps, asg, strategies=None):
-    from .taskgraph import TaskGraph, _bind, _raise_status
+def _eval_encoded(low, maps, asg, strategies=None, with_status=False):
+    """Makespans of encoded strategies.  Raises like build_task_graph for the
+    first failing one, or (``with_status``) returns (makespans, status, low)."""
     n = maps.shape[0]
     mk = np.zeros(n, dtype=np.float64)
     st = np.zeros(n, dtype=np.int32)
@@ -155,14 +156,21 @@ def _eval_encoded(low, maps, asg, strategies=None):
         if not np.any(st == nat.PS_STATUS_CAPACITY):
             break
         low = _regrow(low)  # a ready set outgrew its shared-memory capacity: 4x capacity
+    if with_status:
+        return mk, st, low
     bad = np.nonzero(st)[0]
     if bad.size:
         i = int(bad[0])
-        strat = strategies[i] if strategies is not None else low.decode(maps[i], asg[i])
-        tg = TaskGraph(low.graph, low.topology, strat, low.profile, low.mode)
-        _bind(tg, low)
-        _raise_status(tg, int(st[i]))
+        _raise_for(low, maps[i], asg[i], int(st[i]), strategies[i] if strategies is not None else None)
     return mk
+
+
+def _raise_for(low, map_local, assign, status, strategy=None):
+    from .taskgraph import TaskGraph, _bind, _raise_status
+    strat = strategy if strategy is not None else low.decode(map_local, assign)
+    tg = TaskGraph(low.graph, low.topology, strat, low.profile, low.mode)
+    _bind(tg, low)
+    _raise_status(tg, status)
 
 
 def fit_capacity(low, maps, asg, headroom: int = 1):
@@ -284,7 +292,12 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
             mt[i, 624] = pos
     deterministic = params.budget_seconds is None
     cap = int(params.max_proposals) if params.max_proposals is not None else 0
-    record = cap if deterministic else 0
+    seg = max(1, int(params.segment))
+    if params.check_interval:
+        seg = min(seg, int(params.check_interval)) if not deterministic else int(params.check_interval)
+    # the device keeps a ring of `record` proposals per chain: every proposal of a
+    # fixed-length search, or one segment of a time-boxed one (read after each)
+    record = cap if deterministic else seg
     mp = nat.PsMcmcParams(rng_mode, params.beta is not None, float(params.beta or 0.0), math.log(10.0),
                           1 if record else 0, record)
     h = ctypes.c_void_p()
@@ -292,12 +305,10 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
                                nat.ptr(mt) if mt is not None else None, ctypes.byref(h)), "ps_mcmc_create")
     summ = (nat.PsChainSummary * n)()
     term = ["budget"] * n
+    seg_trace: list[list] = [[] for _ in range(n)]
     try:
         if deterministic:
             done = 0
-            seg = max(1, params.segment)
-            if params.check_interval:
-                seg = int(params.check_interval)
             while True:
                 step = min(cap - done, seg) if cap else 0
                 nat.check(L.ps_mcmc_run(h, step, None), "ps_mcmc_run")
@@ -312,12 +323,29 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
             last_best = np.full(n, np.inf)
             last_improve = np.full(n, t0)
             stopped = np.zeros(n, dtype=bool)
+            copied = np.zeros(n, dtype=np.int64)
+            tc = np.zeros((n, record), dtype=np.float64)
+            tok = np.zeros((n, record), dtype=np.uint8)
             while True:
-                step = max(1, params.segment)
+                step = seg
                 if cap:
-                    step = min(step, cap - int(max((s.proposals for s in summ), default=0)))
-                nat.check(L.ps_mcmc_run(h, max(step, 0), None), "ps_mcmc_run")
-                nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+                    live_props = [summ[i].proposals for i in range(n) if not stopped[i]]
+                    step = min(step, cap - int(max(live_props, default=0)))
+                remaining = params.budget_seconds - (time.monotonic() - t0)
+                if step > 0 and remaining > 0:
+                    # a time-boxed segment: chains stop between proposals once the
+                    # remaining budget is spent (device clock), so a short budget
+                    # does not overrun by a whole segment
+                    nat.check(L.ps_mcmc_run_budget(h, step, max(1, int(remaining * 1e9)), None),
+                              "ps_mcmc_run_budget")
+                nat.check(L.ps_mcmc_read(h, summ, None, None, nat.ptr(tc), nat.ptr(tok)), "ps_mcmc_read")
+                for i in range(n):
+                    p = int(summ[i].proposals)
+                    seg_trace[i].extend((float(tc[i, j % record]), bool(tok[i, j % record]))
+                                        for j in range(int(copied[i]), p))
+                    copied[i] = p
+                if params.check_interval:
+                    _verify_chains(low, h, n, live, summ)
                 now = time.monotonic()
                 halt = np.zeros(n, dtype=np.uint8)
                 for i in range(n):
@@ -339,14 +367,15 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
                     stopped[i] = True
                 if halt.any():
                     nat.check(L.ps_mcmc_stop(h, nat.ptr(halt)), "ps_mcmc_stop")
-                if stopped.all() or all(summ[i].status not in (nat.PS_STATUS_OK,) or stopped[i] for i in range(n)):
+                if all(stopped[i] or summ[i].status != nat.PS_STATUS_OK for i in range(n)):
                     break
         bmaps = np.zeros((n, low.n_ops), dtype=np.int32)
         basg = np.zeros((n, low.n_slots), dtype=np.uint8)
+        det_trace = deterministic and record
         tc = np.zeros((n, max(record, 1)), dtype=np.float64)
         tok = np.zeros((n, max(record, 1)), dtype=np.uint8)
-        nat.check(L.ps_mcmc_read(h, summ, nat.ptr(bmaps), nat.ptr(basg), nat.ptr(tc) if record else None,
-                                 nat.ptr(tok) if record else None), "ps_mcmc_read")
+        nat.check(L.ps_mcmc_read(h, summ, nat.ptr(bmaps), nat.ptr(basg), nat.ptr(tc) if det_trace else None,
+                                 nat.ptr(tok) if det_trace else None), "ps_mcmc_read")
         if any(summ[i].status == nat.PS_STATUS_CAPACITY for i in range(n)):
             return False
         for i, ci in enumerate(live):
@@ -365,9 +394,11 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
                 _logger.warning("chain %d aborted after %d proposals: %s", ci, s.proposals, termination[7:])
             summaries[ci] = ChainSummary(ci, s.initial_cost, s.best_cost, int(s.proposals), int(s.accepted),
                                          s.beta, termination)
-            if record:
+            if det_trace:
                 k = min(int(s.proposals), record)
                 traces[ci] = [(float(tc[i, j]), bool(tok[i, j])) for j in range(k)]
+            elif not deterministic:
+                traces[ci] = seg_trace[i]
             best[ci] = (s.best_cost, low.decode(bmaps[i], basg[i], template=initial[ci]))
     finally:
         L.ps_mcmc_destroy(h)
@@ -423,17 +454,28 @@ def _neighbours(g, topo, maps, devices, op_id, current):
             yield ParallelizationConfig(dict(m.degrees), assignment)
 
 
-def _neighbour_batch(low, op_id, base_m, base_a, cfgs):
+def _neighbour_batch(low, op_id, base_m, base_a, cfgs, best):
+    """Scores single-op neighbours in one GPU batch.  Returns the index of the
+    first neighbour (in scan order) that improves on ``best`` -- with its cost
+    -- or (None, None); a neighbour the reference's update_task_graph would fail
+    on (a missing link) raises, but only when no improving neighbour precedes it
+    (the reference scans sequentially and stops at whichever comes first)."""
     r = low.rank[op_id]
     off = int(low.slot_off[r])
-    op = low.graph.ops[op_id]
     mm = np.repeat(base_m[None], len(cfgs), axis=0)
     aa = np.repeat(base_a[None], len(cfgs), axis=0)
     for j, (t, assignment) in enumerate(cfgs):
         mm[j, r] = low.map_index[r][t]
         for k, dev in enumerate(assignment):
             aa[j, off + k] = low.dev_index[dev]
-    return _eval_encoded(low, mm, aa)
+    costs, st, low2 = _eval_encoded(low, mm, aa, with_status=True)
+    hit = np.nonzero((st != nat.PS_STATUS_OK) | (costs < best))[0]
+    if hit.size == 0:
+        return None, None
+    j = int(hit[0])
+    if st[j] != nat.PS_STATUS_OK:
+        _raise_for(low2, mm[j], aa[j], int(st[j]))
+    return j, float(costs[j])
 
 
 def _greedy_descend(g, topo, profile, strategy, cost, params, batch: int = 4096):
@@ -471,14 +513,12 @@ def _greedy_descend(g, topo, profile, strategy, cost, params, batch: int = 4096)
                     pos = stop
                     continue
                 base_m, base_a = low.encode(current)
-                costs = _neighbour_batch(low, op_id, base_m, base_a, [(full[i][0], full[i][1]) for i in idx])
-                hit = np.nonzero(costs < best)[0]
-                if hit.size == 0:
+                j, cost = _neighbour_batch(low, op_id, base_m, base_a, [(full[i][0], full[i][1]) for i in idx], best)
+                if j is None:
                     pos = stop
                     continue
-                j = int(hit[0])
                 i = idx[j]
-                best = float(costs[j])
+                best = cost
                 t, a, m = full[i]
                 current.configs[op_id] = ParallelizationConfig(dict(m.degrees), a)
                 cur_key = (t, a)
@@ -521,12 +561,10 @@ def local_optimality_check(strategy: ParallelizationStrategy, g: OperatorGraph, 
             chunk = list(islice(gen, batch))
             if not chunk:
                 break
-            costs = _neighbour_batch(low, op_id, base_m, base_a, [(t, a) for t, a, _ in chunk])
-            hit = np.nonzero(costs < base)[0]
-            if hit.size:
-                j = int(hit[0])
+            j, cost = _neighbour_batch(low, op_id, base_m, base_a, [(t, a) for t, a, _ in chunk], base)
+            if j is not None:
                 t, a, m = chunk[j]
-                return op_id, ParallelizationConfig(dict(m.degrees), a), float(costs[j])
+                return op_id, ParallelizationConfig(dict(m.degrees), a), cost
     return None
 
 

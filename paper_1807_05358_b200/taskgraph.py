@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -173,29 +174,55 @@ class TaskGraph:
 # -----------------------------------------------------------------------------
 # strategy-backed construction
 
-_LOWER_CACHE_ATTR = "_b200_lowered"
+# Lowered problems cached per profile object, outside the profile (so the profile
+# still pickles and deep-copies).  An entry is reused only while its fingerprint
+# -- the graph's ops and tensors, the topology's devices and connections, the
+# profile's entries, fallback and backward multiplier, the mode -- is unchanged:
+# an in-place edit of any of them lowers again, as the reference would pick the
+# new values up on its next build.
+_LOWER_CACHE: dict = {}
+
+
+def _fingerprint(g, topo, profile, mode):
+    return (id(g), tuple(map(id, g.ops.values())), tuple(map(id, g.tensors)), id(topo),
+            tuple(map(id, topo.devices.values())), tuple(map(id, topo.connections)), mode,
+            profile.backward_multiplier, repr(profile.fallback), len(profile.entries),
+            hash(frozenset(profile.entries.items())))
+
+
+def _cache_get(profile):
+    hit = _LOWER_CACHE.get(id(profile))
+    if hit is None or hit[0]() is not profile:
+        return None
+    return hit
+
+
+def _cache_put(profile, fp, low, strategies):
+    pid = id(profile)
+    try:
+        ref = weakref.ref(profile, lambda _r, pid=pid: _LOWER_CACHE.pop(pid, None))
+    except TypeError:
+        return
+    _LOWER_CACHE[pid] = (ref, fp, low, strategies)
 
 
 def _problem_for(g, topo, profile, mode, strategy, max_degree=None) -> Lowered:
     """Reuse a lowered problem for (g, topo, profile, mode) when it covers the
     strategy's degree maps; otherwise lower again (union of maps)."""
-    cache = getattr(profile, "__dict__", {}).get(_LOWER_CACHE_ATTR)
-    key = (id(g), len(g.ops), len(g.tensors), id(topo), len(topo.devices), len(topo.connections), mode,
-           profile.backward_multiplier)
-    if cache is not None and cache[0] == key:
-        low = cache[1]
+    hit = _cache_get(profile)
+    fp = _fingerprint(g, topo, profile, mode)
+    if hit is not None and hit[1] == fp:
+        low = hit[2]
         if (max_degree is None or low.max_degree == max_degree) and low.has_maps_for(strategy):
             return low
-        strategies = [strategy] + cache[2]
+        strategies = [strategy] + hit[3]
+        if max_degree is None:
+            max_degree = low.max_degree
     else:
         strategies = [strategy]
-    low = lower(g, topo, profile, mode, max_degree=max_degree if max_degree is not None else
-                (cache[1].max_degree if cache is not None and cache[0] == key else None),
-                strategies=strategies)
-    try:
-        profile.__dict__[_LOWER_CACHE_ATTR] = (key, low, strategies[-8:])
-    except (AttributeError, TypeError):
-        pass
+    low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=strategies)
+    # lowering inserts the fallback's answers into profile.entries: fingerprint after
+    _cache_put(profile, _fingerprint(g, topo, profile, mode), low, strategies[-8:])
     return low
 
 
@@ -330,12 +357,9 @@ def build_task_graph(g: OperatorGraph, topo: DeviceTopology, strategy: Paralleli
 def _grow(tg: TaskGraph):
     from .search import _regrow
     new = _regrow(tg._low)
-    try:
-        cache = tg.profile.__dict__.get(_LOWER_CACHE_ATTR)
-        if cache is not None and cache[1] is tg._low:
-            tg.profile.__dict__[_LOWER_CACHE_ATTR] = (cache[0], new, cache[2])
-    except (AttributeError, TypeError):
-        pass
+    hit = _cache_get(tg.profile)
+    if hit is not None and hit[2] is tg._low:
+        _LOWER_CACHE[id(tg.profile)] = (hit[0], hit[1], new, hit[3])
     _bind(tg, new)
 
 

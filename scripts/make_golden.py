@@ -181,8 +181,96 @@ def rnn3_case():
     return doc
 
 
+def timeline_digest(table) -> str:
+    """sha256 over the sorted (origin, start, end, device) rows of timeline_table
+    (tests/golden_io.timeline_digest computes the same on the GPU side)."""
+    import hashlib
+    rows = sorted((repr(tuple(o)), H(s), H(e), d) for o, (s, e, d) in table.items())
+    return hashlib.sha256(json.dumps(rows, separators=(",", ":")).encode()).hexdigest()
+
+
+def graph_digest(doc) -> str:
+    import hashlib
+    return hashlib.sha256(json.dumps(doc, sort_keys=True, separators=(",", ":")).encode()).hexdigest()
+
+
+def large_cases():
+    """The BASELINE configs at their full sizes (64 devices; 1k- and 10k-op random
+    DAGs), simulated by the reference itself.  Inputs are generated by this
+    package's workload generators (the reference has none for these shapes) and
+    pinned by a digest of their JSON; outputs are makespans, counts and a digest
+    of the whole timeline."""
+    specs = [("resnet101_16x4", lambda: W.resnet101(), lambda: W.multi_node_topology(16, 4), 8, 3),
+             ("nmt40_16x4", lambda: W.nmt_like(steps=40, layers=2, batch=64, hidden=1024, vocab=32768),
+              lambda: W.multi_node_topology(16, 4), 8, 3),
+             ("random1k_4x4", lambda: W.random_dag(1000, seed=1000), lambda: W.multi_node_topology(4, 4), 4, 3),
+             ("random10k_4x4", lambda: W.random_dag(10000, seed=1000), lambda: W.multi_node_topology(4, 4), 4, 2)]
+    out = []
+    for name, mk_g, mk_t, md, n_rand in specs:
+        gdoc, tdoc = W_json(mk_g()), W_topo_json(mk_t())
+        g = R.graph_from_json(gdoc)
+        topo = R.topology_from_json(tdoc)
+        strategies = [R.data_parallel_strategy(g, topo)] + [R.random_strategy(g, topo, md, s) for s in range(n_rand)]
+        for mode in (R.MODE_FORWARD, R.MODE_FULL):
+            recs = []
+            for st in strategies:
+                tg = R.build_task_graph(g, topo, st, R.CostProfile(), mode)
+                res = R.full_simulate(tg)
+                recs.append({"makespan": H(res.makespan), "tasks": len(tg.tasks),
+                             "comm_tasks": sum(1 for t in tg.tasks.values() if t.kind == "comm"),
+                             "edges": sum(len(t.outputs) for t in tg.tasks.values()),
+                             "comm_bytes": H(float(tg.total_comm_bytes)),
+                             "timeline_sha256": timeline_digest(R.timeline_table(tg))})
+                print(name, mode, recs[-1]["tasks"], flush=True)
+            out.append({"name": name, "mode": mode, "max_degree": md, "graph_sha256": graph_digest(gdoc),
+                        "topology": tdoc, "random_seeds": list(range(n_rand)), "results": recs})
+    return out
+
+
+def profile_cases():
+    """Measured-profile path (cost.py:105-121,136-198): a profile text with
+    entries for some keys (perturbed analytic times), a fallback with its own
+    rate and a nonzero overhead for the rest, and a non-default backward
+    multiplier; simulated by the reference."""
+    out = []
+    specs = [("alexnet_1x4", lambda: W.alexnet_like(), lambda: W.single_node_topology(4), 4),
+             ("inception_4x4", lambda: W.inception_v3(), lambda: W.multi_node_topology(4, 4), 4)]
+    for name, mk_g, mk_t, md in specs:
+        gdoc, tdoc = W_json(mk_g()), W_topo_json(mk_t())
+        g = R.graph_from_json(gdoc)
+        topo = R.topology_from_json(tdoc)
+        strategies = [R.data_parallel_strategy(g, topo)] + [R.random_strategy(g, topo, md, s) for s in range(4)]
+        # measured entries: every third key the analytic model produces, times 1.37 / 0.61
+        probe = R.CostProfile()
+        for st in strategies:
+            R.build_task_graph(g, topo, st, probe, R.MODE_FULL)
+        keys = sorted(probe.entries, key=lambda k: (k.kind, k.digest, k.region_dims, k.device_kind))
+        measured = R.CostProfile()
+        for i, k in enumerate(keys):
+            if i % 3 == 0:
+                measured.entries[k] = probe.entries[k] * (1.37 if i % 2 else 0.61)
+        text = R.dumps_profile(measured)
+        fallback = {"throughput": {"gpu": 4.0e11}, "default_throughput": 1.0e12, "overhead": 3.5e-6}
+        for mode in (R.MODE_FORWARD, R.MODE_FULL):
+            prof = R.loads_profile(text, R.AnalyticCostModel(**fallback))
+            prof.backward_multiplier = 2.5
+            mks = [H(R.full_simulate(R.build_task_graph(g, topo, st, prof, mode)).makespan) for st in strategies]
+            out.append({"name": name, "mode": mode, "max_degree": md, "graph": gdoc, "topology": tdoc,
+                        "strategies": [R.strategy_to_json(s) for s in strategies], "profile_text": text,
+                        "fallback": fallback, "backward_multiplier": 2.5, "makespans": mks,
+                        "fallback_evaluations": prof.fallback_evaluations})
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--large" in sys.argv:  # the full-size / measured-profile fixtures only
+        docs = {"simulate_large.json": large_cases(), "profiles.json": profile_cases()}
+        for name, doc in docs.items():
+            with open(os.path.join(OUT, name), "w") as fh:
+                json.dump(doc, fh, separators=(",", ":"))
+            print("wrote", name, os.path.getsize(os.path.join(OUT, name)))
+        return
     docs = {"rnn3_model_parallel.json": rnn3_case(), "simulate_random.json": simulate_cases(),
             "simulate_benchmarks.json": benchmark_cases(), "mcmc.json": mcmc_cases(),
             "search_reports.json": search_report_cases(), "exhaustive.json": exhaustive_cases()}

@@ -71,3 +71,38 @@ def test_mt19937_matches_cpython(oracle):
     for seed in (0, 1, 1000003, 2 ** 32 + 5):
         r = random.Random(seed)
         assert oracle.rng_words("mt", seed, 700) == [r.getrandbits(32) for _ in range(700)]
+
+
+def _oracle_table(res, topo):
+    names = __import__("golden_io").queue_names(topo)
+    return {o: (v[1], v[2], names[v[3]]) for o, v in res["timeline"].items()}
+
+
+@pytest.mark.parametrize("name", ["resnet101_16x4", "nmt40_16x4", "random1k_4x4", "random10k_4x4"])
+def test_oracle_matches_reference_at_full_size(oracle, name):
+    """The BASELINE configs at full size (64 devices, 1k/10k-op DAGs): makespan,
+    counts, byte totals and the whole timeline (digest) equal the reference's."""
+    from golden_io import large_inputs, timeline_digest
+    for doc in (d for d in load("simulate_large.json") if d["name"] == name):
+        g, topo, strategies = large_inputs(doc)
+        for s, rec in zip(strategies, doc["results"]):
+            got = oracle.simulate(g, topo, ps.CostProfile(), doc["mode"], s, cap=1 << 28)
+            assert got["makespan"] == fx(rec["makespan"]), (name, doc["mode"])
+            assert (got["tasks"], got["comm_tasks"], got["edges"]) == (rec["tasks"], rec["comm_tasks"], rec["edges"])
+            assert got["comm_bytes"] == fx(rec["comm_bytes"])
+            assert timeline_digest(_oracle_table(got, topo)) == rec["timeline_sha256"], (name, doc["mode"])
+
+
+def _profile_of(doc):
+    prof = ps.loads_profile(doc["profile_text"], ps.AnalyticCostModel(**doc["fallback"]))
+    prof.backward_multiplier = doc["backward_multiplier"]
+    return prof
+
+
+def test_oracle_matches_reference_with_a_measured_profile(oracle):
+    """Profile-text entries + a fallback with its own rate and overhead + a
+    non-default backward multiplier (cost.py:105-121,136-198)."""
+    for doc in load("profiles.json"):
+        g, topo, strategies = inputs(doc)
+        got = oracle.makespans(g, topo, _profile_of(doc), doc["mode"], strategies)
+        assert [float(x) for x in got] == [fx(h) for h in doc["makespans"]], (doc["name"], doc["mode"])

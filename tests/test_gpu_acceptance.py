@@ -1,0 +1,137 @@
+"""Acceptance-scale GPU parity (reference pkg/tests/test_acceptance.py) and the
+BASELINE configs at full size against vectors produced by the reference itself
+(tests/golden/simulate_large.json, profiles.json; scripts/make_golden.py --large)."""
+
+import random
+
+import numpy as np
+import pytest
+
+import paper_1807_05358_b200 as ps
+from golden_io import fx, inputs, large_inputs, load, timeline_digest
+from helpers import random_graph, random_topology
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["resnet101_16x4", "nmt40_16x4", "random1k_4x4", "random10k_4x4"])
+def test_full_size_configs_match_the_reference(name):
+    """Makespans, counts, byte totals and whole timelines of the BASELINE configs
+    at full size equal the reference's own (no oracle in between)."""
+    for doc in (d for d in load("simulate_large.json") if d["name"] == name):
+        g, topo, strategies = large_inputs(doc)
+        prof = ps.CostProfile()
+        got = ps.evaluate_strategies(g, topo, prof, strategies, mode=doc["mode"], max_degree=doc["max_degree"])
+        assert [float(x) for x in got] == [fx(r["makespan"]) for r in doc["results"]], (name, doc["mode"])
+        # whole timelines through the TaskGraph API (traced GPU simulation)
+        for s, rec in list(zip(strategies, doc["results"]))[:2 if name == "random10k_4x4" else None]:
+            tg = ps.build_task_graph(g, topo, s, prof, doc["mode"])
+            assert ps.full_simulate(tg).makespan == fx(rec["makespan"])
+            assert len(tg.tasks) == rec["tasks"]
+            assert sum(1 for t in tg.tasks.values() if t.kind == "comm") == rec["comm_tasks"]
+            assert sum(len(t.outputs) for t in tg.tasks.values()) == rec["edges"]
+            assert tg.total_comm_bytes == fx(rec["comm_bytes"])
+            assert timeline_digest(ps.timeline_table(tg)) == rec["timeline_sha256"], (name, doc["mode"])
+
+
+def test_measured_profile_matches_the_reference():
+    """Profile-text entries, a fallback with its own rate and overhead, backward
+    multiplier 2.5: batch makespans and MCMC against the oracle."""
+    for doc in load("profiles.json"):
+        g, topo, strategies = inputs(doc)
+        prof = ps.loads_profile(doc["profile_text"], ps.AnalyticCostModel(**doc["fallback"]))
+        prof.backward_multiplier = doc["backward_multiplier"]
+        got = ps.evaluate_strategies(g, topo, prof, strategies, mode=doc["mode"], max_degree=doc["max_degree"])
+        assert [float(x) for x in got] == [fx(h) for h in doc["makespans"]], (doc["name"], doc["mode"])
+        tg = ps.build_task_graph(g, topo, strategies[1], prof, doc["mode"])
+        assert ps.full_simulate(tg).makespan == fx(doc["makespans"][1])
+
+
+def test_measured_profile_mcmc_matches_oracle(oracle):
+    doc = load("profiles.json")[3]  # inception, full-iteration
+    g, topo, strategies = inputs(doc)
+
+    def prof():
+        p = ps.loads_profile(doc["profile_text"], ps.AnalyticCostModel(**doc["fallback"]))
+        p.backward_multiplier = doc["backward_multiplier"]
+        return p
+    init = strategies[:4]
+    rep = ps.mcmc_search(g, topo, prof(), ps.SearchParams(max_proposals=150, seed=3, max_degree=4, mode=doc["mode"],
+                                                          initial=init, polish=False, rng="philox"))
+    ref = oracle.mcmc(g, topo, prof(), doc["mode"], init, [3 + 1000003 * c for c in range(4)], 150, 4,
+                      rng_mode="philox")
+    for ci, ch in enumerate(rep.chains):
+        assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted, ch.beta) == tuple(ref["summary"][ci][:5])
+
+
+def test_zero_task_times_match_oracle(oracle):
+    """Zero-time tasks (legal in the reference) exercise the degenerate-round path."""
+    for seed in range(6):
+        rng = random.Random(777 + seed)
+        g = random_graph(rng, 6, 14)
+        topo = random_topology(rng, rng.choice((2, 4, 8)))
+        prof = ps.CostProfile(fallback=ps.AnalyticCostModel(default_throughput=float("inf")))
+        mode = ps.MODE_FULL if seed % 2 else ps.MODE_FORWARD
+        strategies = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, 3, seed * 7 + i)
+                                                            for i in range(4)]
+        got = ps.evaluate_strategies(g, topo, prof, strategies, mode=mode, max_degree=3)
+        assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies)), seed
+
+
+def test_criterion_3_full_simulate_matches_the_oracle_on_500_graphs(oracle):
+    """test_acceptance.py:125-142: 500 random task graphs; build_task_graph +
+    full_simulate on the GPU == oracle_simulate (explicit-graph kernel) == the C
+    oracle (pinned to the reference)."""
+    for seed in range(500):
+        rng = random.Random(20000 + seed)
+        g = random_graph(rng)
+        topo = random_topology(rng, rng.choice((2, 4, 8, 16)))
+        mode = ps.MODE_FULL if seed % 2 else ps.MODE_FORWARD
+        s = ps.random_strategy(g, topo, rng.choice((2, 3)), seed)
+        prof = ps.CostProfile()
+        tg = ps.build_task_graph(g, topo, s, prof, mode)
+        mk = ps.full_simulate(tg).makespan
+        assert mk == oracle.makespans(g, topo, prof, mode, [s])[0], seed
+        if seed % 10 == 0:
+            assert ps.oracle_simulate(tg) == mk, seed
+
+
+def _random_single_op_change(rng, g, topo, max_degree):
+    op_id = rng.choice(sorted(g.ops))
+    cfg = rng.choice(ps.enumerate_configs(g.ops[op_id], topo, max_degree))
+    assignment = tuple(rng.choice(topo.device_ids()) for _ in range(cfg.size()))
+    return op_id, ps.ParallelizationConfig(dict(cfg.degrees), assignment)
+
+
+def test_criterion_1_delta_equals_a_fresh_build_on_10000_changes(oracle):
+    """test_acceptance.py:55-87 at its own scale: 10,000 chained single-op changes
+    over 2-64 devices through update_task_graph + delta_simulate; every makespan
+    equals a fresh build_task_graph + full_simulate and the C oracle, and whole
+    timelines are compared every 25th change and at the end of each scenario."""
+    device_span = (2, 4, 8, 16, 32, 64)
+    triples = scenario = 0
+    while triples < 10000:
+        rng = random.Random(9000 + scenario)
+        g = random_graph(rng)
+        devs = device_span[scenario % len(device_span)]
+        topo = random_topology(rng, devs)
+        mode = ps.MODE_FULL if scenario % 2 else ps.MODE_FORWARD
+        prof = ps.CostProfile()
+        tg = ps.build_task_graph(g, topo, ps.random_strategy(g, topo, 4, scenario), prof, mode)
+        ps.full_simulate(tg)
+        seen, got = [], []
+        for step in range(250):
+            op_id, cfg = _random_single_op_change(rng, g, topo, 4)
+            _, changed = ps.update_task_graph(tg, g, topo, op_id, cfg)
+            res = ps.delta_simulate(tg, changed)
+            seen.append(tg.strategy.copy())
+            got.append(res.makespan)
+            if step % 25 == 24:
+                fresh = ps.build_task_graph(g, topo, tg.strategy, prof, mode)
+                assert res.makespan == ps.full_simulate(fresh).makespan, (scenario, step)
+                assert ps.timeline_table(tg) == ps.timeline_table(fresh), (scenario, step)
+            triples += 1
+        fresh = ps.evaluate_strategies(g, topo, prof, seen, mode=mode, max_degree=4)
+        assert got == [float(x) for x in fresh], scenario
+        assert got == [float(x) for x in oracle.makespans(g, topo, prof, mode, seen)], scenario
+        scenario += 1

@@ -332,7 +332,7 @@ def test_bench_config_mcmc_matches_oracle(oracle):
     import os
     g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
     prof = ps.CostProfile()
-    C, P = 1024, 6
+    C, P = 1024, 128
     init = [ps.data_parallel_strategy(g, topo)] + [ps.random_strategy(g, topo, md, c) for c in range(1, C)]
     seeds = [1000003 * c for c in range(C)]
     params = ps.SearchParams(max_proposals=P, seed=0, max_degree=md, mode=ps.MODE_FULL, initial=init,

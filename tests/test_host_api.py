@@ -282,3 +282,46 @@ def test_random_strategies_batch_equals_single_draws():
         one = ps.random_strategy(g, topo, 4, s)
         assert {k: (c.degrees, c.assignment) for k, c in one.configs.items()} == \
             {k: (c.degrees, c.assignment) for k, c in b.configs.items()}
+
+
+# -- lowering cache and task-time validation (host side) --------------------------
+
+def test_lowering_cache_tracks_in_place_edits_and_keeps_profile_picklable():
+    import copy
+    import pickle
+    from paper_1807_05358_b200.taskgraph import _problem_for
+    g = ps.alexnet_like()
+    topo = ps.single_node_topology(4)
+    prof = ps.CostProfile()
+    s = ps.data_parallel_strategy(g, topo)
+    a = _problem_for(g, topo, prof, ps.MODE_FULL, s)
+    assert _problem_for(g, topo, prof, ps.MODE_FULL, s) is a  # cache hit
+    # the cache lives outside the profile: it still pickles and deep-copies
+    pickle.loads(pickle.dumps(prof))
+    copy.deepcopy(prof)
+    # an in-place edit of a profile entry lowers again with the new value
+    key = next(iter(prof.entries))
+    prof.entries[key] = prof.entries[key] * 3.0
+    b = _problem_for(g, topo, prof, ps.MODE_FULL, s)
+    assert b is not a and key in prof.entries
+    assert _problem_for(g, topo, prof, ps.MODE_FULL, s) is b
+    # so does a changed link (a new Connection registered on the topology)
+    topo.connections.append(ps.Connection("gpu0", "gpu1", 1.0, 0.0))
+    assert _problem_for(g, topo, prof, ps.MODE_FULL, s) is not b
+    # and a replaced operation
+    oid = sorted(g.ops)[0]
+    op = g.ops[oid]
+    g.ops[oid] = ps.Operation(op.id, op.kind, op.input_shapes, op.output_shape, op.param_bytes + 4)
+    c = _problem_for(g, topo, prof, ps.MODE_FULL, s)
+    assert _problem_for(g, topo, prof, ps.MODE_FULL, s) is c
+
+
+def test_negative_task_times_are_rejected_by_the_lowering():
+    g = ps.alexnet_like()
+    topo = ps.single_node_topology(4)
+    prof = ps.CostProfile(fallback=ps.AnalyticCostModel(overhead=-1.0))
+    with pytest.raises(ValueError, match="negative"):
+        lower(g, topo, prof, ps.MODE_FORWARD, max_degree=2)
+    # zero times are legal (the reference schedules them; the GPU replay is exact for them)
+    lower(g, topo, ps.CostProfile(fallback=ps.AnalyticCostModel(default_throughput=math.inf)), ps.MODE_FORWARD,
+          max_degree=2)
