@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--mode", default="full-iteration", choices=("forward", "full-iteration"))
     ap.add_argument("--config", default="inception", choices=("inception", "alexnet", "resnet", "nmt", "random"))
     ap.add_argument("--ops", type=int, default=1000, help="operator count of the random-DAG config")
+    ap.add_argument("--no-delta", action="store_true",
+                    help="score every proposal from time zero instead of resuming from a snapshot")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -223,7 +225,7 @@ def run_ours(args):
     low = fit_capacity(low, maps, asg)  # ready-set capacity from a pilot evaluation of the starts
     info = low.info()
     seeds = np.array([1000003 * (first + i) for i in range(C)], dtype=np.uint64)
-    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0)
+    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0, 0 if args.no_delta else 1)
     h = ctypes.c_void_p()
     nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
                                ctypes.byref(h)), "ps_mcmc_create")
@@ -282,6 +284,8 @@ def run_ours(args):
     summ = (nat.PsChainSummary * C)()
     nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
     evals = sum(s.proposals for s in summ) - props0
+    rounds_run = sum(s.rounds_run for s in summ) - sum(s.rounds_run for s in summ0)
+    rounds_reused = sum(s.rounds_reused for s in summ) - sum(s.rounds_reused for s in summ0)
     bad = sum(1 for s in summ if s.status != nat.PS_STATUS_OK)
     # best strategy across chains: device argmin, then the one cross-GPU exchange
     from paper_1807_05358_b200.parallel import global_best
@@ -404,6 +408,8 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
+        "delta": {"enabled": not args.no_delta, "rounds_run": int(rounds_run), "rounds_reused": int(rounds_reused),
+                  "reused_fraction": rounds_reused / max(1, rounds_run + rounds_reused)},
         "chain_failures": bad, "best_makespan": float(best.item()), "best_chain": win_chain,
         "full_eval": {"value": full_value, "unit": UNIT, "candidates_per_launch": FB, "failures": bad_full,
                       "note": "full evaluations (no search) of the chains' current strategies (8 adjacent copies each), "

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 1
+#define PS_ABI_VERSION 2
 #define PS_MAXDIM 5
 
 enum {
@@ -166,6 +166,10 @@ typedef struct ps_mcmc_params {
   double ln10;            /* math.log(10.0) of the host */
   int32_t record_trace;   /* keep (cand, accepted) per proposal */
   int32_t trace_capacity; /* ring of proposals recorded per chain: proposal i lands in slot i % capacity */
+  int32_t delta;          /* 1: checkpointed delta evaluation of proposals (update_task_graph +
+                             delta_simulate, taskgraph.py:309-418, simulate.py:120-210); 0: each
+                             proposal re-simulates from time zero.  Same results either way. */
+  int32_t reserved_;
 } ps_mcmc_params;
 
 typedef struct ps_chain_summary {
@@ -174,6 +178,8 @@ typedef struct ps_chain_summary {
   int32_t status;         /* PS_STATUS_* of the chain */
   int32_t err_a, err_b;   /* device pair of a no-route failure */
   int32_t last_op;        /* op of the most recent proposal */
+  int64_t rounds_run;     /* simulation rounds executed (delta evaluation) */
+  int64_t rounds_reused;  /* rounds skipped by resuming from a snapshot */
 } ps_chain_summary;
 
 typedef struct ps_mcmc ps_mcmc;

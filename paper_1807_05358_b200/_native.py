@@ -21,7 +21,7 @@ PS_OK, PS_ERR_INVALID, PS_ERR_NO_ROUTE, PS_ERR_CYCLE, PS_ERR_CAPACITY, PS_ERR_CU
 PS_STATUS_OK, PS_STATUS_NO_ROUTE, PS_STATUS_CAPACITY, PS_STATUS_STOPPED = 0, 2, 4, 9
 PS_HOST_PTRS, PS_DEVICE_PTRS = 0, 1
 PS_RNG_PHILOX, PS_RNG_MT19937 = 0, 1
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 c_int_p = ctypes.POINTER(ctypes.c_int32)
 c_i64_p = ctypes.POINTER(ctypes.c_int64)
@@ -71,14 +71,18 @@ TRACE_DTYPE = np.dtype([("key", np.uint64), ("queue", np.int32), ("aux", np.int3
 
 class PsMcmcParams(ctypes.Structure):
     _fields_ = [("rng_mode", ctypes.c_int32), ("beta_given", ctypes.c_int32), ("beta", ctypes.c_double),
-                ("ln10", ctypes.c_double), ("record_trace", ctypes.c_int32), ("trace_capacity", ctypes.c_int32)]
+                ("ln10", ctypes.c_double), ("record_trace", ctypes.c_int32), ("trace_capacity", ctypes.c_int32),
+                ("delta", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
+
+    def __init__(self, rng_mode=0, beta_given=0, beta=0.0, ln10=0.0, record_trace=0, trace_capacity=0, delta=1):
+        super().__init__(rng_mode, beta_given, beta, ln10, record_trace, trace_capacity, delta, 0)
 
 
 class PsChainSummary(ctypes.Structure):
     _fields_ = [("initial_cost", ctypes.c_double), ("best_cost", ctypes.c_double), ("cost", ctypes.c_double),
                 ("beta", ctypes.c_double), ("proposals", ctypes.c_int64), ("accepted", ctypes.c_int64),
                 ("status", ctypes.c_int32), ("err_a", ctypes.c_int32), ("err_b", ctypes.c_int32),
-                ("last_op", ctypes.c_int32)]
+                ("last_op", ctypes.c_int32), ("rounds_run", ctypes.c_int64), ("rounds_reused", ctypes.c_int64)]
 
 
 _lib = None

@@ -89,6 +89,11 @@ struct DevProb {
   // transfer's time instead of dividing.
   int n_cls;
   double cls_lat[2], cls_bw[2];
+  // delta (checkpoint) evaluation: an upper bound of the dense ring-counter count,
+  // and the smallest time any task can take (0: a zero-time task exists, so the
+  // prefix-reuse argument does not hold and every evaluation runs from scratch)
+  int n_rings;
+  double min_exe;
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
@@ -353,6 +358,81 @@ struct Lay {  // sizes shared by host and device
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// ---------------------------------------------------------------- delta
+// Checkpointed ("delta") evaluation, the B200 form of the reference's
+// update_task_graph + delta_simulate (taskgraph.py:309-418, simulate.py:120-210).
+//
+// A simulation of strategy S records, every `stride` rounds, a snapshot of its
+// state at the round boundary -- queue clocks, ready set, and per task counter
+// the arrivals so far and the running ready time -- plus, per op, the first
+// round in which one of its forward / backward tasks ran.  A single-op change at
+// op o leaves every task that ran before the first round R_o in which a task with
+// an o-dependent successor list ran (o's producers' forward tasks, o's own tasks,
+// o's consumers' backward tasks) bit-identical, and touches no counter or ready
+// entry of the state at that boundary except o's own (provided every task takes
+// a positive time that is not absorbed into its start: then every task the
+// change adds or rewires becomes ready strictly after every task already run).
+// The changed strategy therefore resumes from the last snapshot at or before R_o
+// (its counters rebuilt from the new in-degrees minus the recorded arrivals)
+// instead of from time zero.  A source op (no producers) always runs from scratch.
+// Arrivals, not remaining counts, are recorded, so snapshots stay valid for a
+// later strategy that changed only ops whose tasks had not started at that point:
+// an accepted proposal keeps the snapshots before its resume point and replaces
+// the ones after it.
+struct __align__(16) SnapHdr {
+  int round, n, Tf, G;
+  double makespan;
+  int valid, pad_[9];
+};
+
+struct SnapLay { size_t fb, gb, qc, rs, rd, ar, total; };
+
+__host__ __device__ inline size_t snap_counters(const DevProb &P) {
+  return P.full ? 2 * (size_t)P.n_slots + (size_t)P.n_rings : (size_t)P.n_slots;
+}
+
+__host__ __device__ inline SnapLay snap_layout(const DevProb &P) {
+  SnapLay L;
+  size_t o = sizeof(SnapHdr);
+  L.fb = o; o += al16(4 * (size_t)(P.n_ops + 1));
+  L.gb = o; o += al16(4 * (size_t)(P.n_ops + 1));
+  L.qc = o; o += al16(8 * (size_t)P.n_queues);
+  L.rs = o; o += al16(32 * (size_t)P.cap);
+  L.rd = o; o += al16(8 * snap_counters(P));
+  L.ar = o; o += al16(2 * snap_counters(P));
+  L.total = al16(o);
+  return L;
+}
+
+// Per-chain delta bookkeeping (global; k_mcmc keeps it across launches)
+struct ChainDelta {
+  int stride, nvalid;      // snapshot spacing; indices [1, nvalid) are valid for the current strategy
+  unsigned cur, bad;       // bit i: copy holding index i / index i unusable
+  int fsel, pad_;          // which first-round buffer belongs to the current strategy
+  long long rounds_run, rounds_reused;
+};
+
+// Per-simulation delta context, in the warp's shared-memory slice.
+struct DeltaCtx {
+  char *snap;              // this chain's snapshot slots: index i, copy b at snap + (2 i + b) snap_bytes
+  const char *restore;     // snapshot to resume from (null: from time zero)
+  int *frnd, *brnd;        // this simulation's first round per op (forward / backward tasks)
+  unsigned short *indeg;   // this simulation's dense counter in-degrees (global)
+  unsigned long long snap_bytes;
+  int stride, nsnap;       // rounds between snapshots; snapshot indices per copy
+  unsigned out_sel;        // bit i: the copy index i is written to
+  int op;                  // the changed op (its counters start fresh on resume)
+  int restore_idx;         // index of the resumed snapshot (0: none)
+  int last;                // out: last snapshot index written
+  unsigned bad;            // out: indices whose state did not fit a snapshot
+  int rounds;              // out: round count at the end (resumed rounds included)
+  int r0;                  // round of the resumed snapshot
+  const int *fsrc, *bsrc;  // first rounds of the strategy resumed from (kept below r0)
+  ChainDelta ch;           // k_mcmc: the chain's bookkeeping while the kernel runs
+};
+
+
+
 __host__ __device__ inline size_t tab_bytes_of(const DevProb &P) {
   size_t b = 0;
   b += al16(4 * (size_t)(P.n_ops + 1)) * 4;          // slot_off, map_off, in_off, out_off
@@ -375,6 +455,7 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
   b += 256 + 128 + 16;                               // proposal staging, phase counters
+  b += al16(sizeof(DeltaCtx));                       // delta context
   return b;
 }
 
@@ -400,6 +481,7 @@ struct W2 {
   int *srow, *scol;
   unsigned char *oldasg;
   unsigned long long *ph;  // per-warp phase counters (PS_PHASES builds)
+  DeltaCtx *dc;            // SIM_SNAP simulations: snapshots / resume
 };
 
 __device__ inline void carve_tab(char *base, const DevProb &P, Tab &t) {
@@ -480,6 +562,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.scol = (int *)take(4 * L.RC);
   w.oldasg = (unsigned char *)take(256);
   w.ph = (unsigned long long *)take(128);
+  w.dc = (DeltaCtx *)take(sizeof(DeltaCtx));
   w.rcap = P.cap;
   w.opmin = nullptr;
   w.tr = nullptr;
@@ -542,9 +625,24 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
 // simulator variants: SIM_TRACE records every task and dependency
 // (k_simulate_trace), SIM_OPMIN keeps each op's earliest forward end (exhaustive
 // search bounds); the MCMC kernel compiles neither
-enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4, SIM_FULL = 8, SIM_FWD = 16 };
+enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4, SIM_FULL = 8, SIM_FWD = 16, SIM_SNAP = 32 };
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
+
+// First rounds of a delta simulation: the resumed strategy's below the resume
+// round (those ops ran identically), unset above it.
+__device__ inline void delta_first_rounds(const DevProb &P, DeltaCtx *dc, int lane) {
+  __syncwarp();
+  const int r0 = dc->r0;
+  const int *fs = dc->fsrc, *bs = dc->bsrc;
+  int *fd = dc->frnd, *bd = dc->brnd;
+  for (int i = lane; i < P.n_ops; i += 32) {
+    int a = fs ? fs[i] : 0x7fffffff, b = bs ? bs[i] : 0x7fffffff;
+    fd[i] = a < r0 ? a : 0x7fffffff;
+    bd[i] = b < r0 ? b : 0x7fffffff;
+  }
+  __syncwarp();
+}
 
 // Simulate; a candidate whose ready set outgrows shared memory is re-run with
 // the ready set in global memory (same answer, slower).
@@ -556,6 +654,7 @@ __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &
   W2 wg = w;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
+    if (M & SIM_SNAP) delta_first_rounds(P, w.dc, lane);
     o = warp_simulate2<M>(P, T, wg, L, gscratch, lane);
     if (o.status != PS_STATUS_CAPACITY) break;
     wg = with_global_ready_set(P, gscratch, w);
@@ -798,9 +897,49 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
   return 0.0;
 }
 
+// Snapshot of the simulation state at the start of round `round` (index i):
+// queue clocks, ready set, running makespan, and per dense counter its ready
+// time and arrivals so far (in-degree minus remaining), with the dense layout
+// (fbase / gbase) they are indexed by.  A ready set larger than the resume
+// capacity marks the index unusable.
+__device__ __noinline__ void snap_write(const DevProb &P, const W2 &w, const State &st, int n, int round, int i,
+                                        double mk, bool full, int lane) {
+  DeltaCtx *dc = w.dc;
+  const SnapLay sl = snap_layout(P);
+  char *dst = dc->snap + (2ull * (unsigned)i + ((dc->out_sel >> i) & 1u)) * dc->snap_bytes;
+  unsigned long long mb = (unsigned long long)__double_as_longlong(mk);
+  unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
+  unsigned lo = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32) == hi ? (unsigned)mb : 0u);
+  bool ok = n <= P.cap;
+  if (lane == 0) {
+    SnapHdr h;
+    h.round = round; h.n = n; h.Tf = st.Tf; h.G = st.G;
+    h.makespan = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+    h.valid = ok;
+    *(SnapHdr *)dst = h;
+    dc->last = i;
+    if (!ok) dc->bad |= 1u << i;
+  }
+  if (!ok) return;
+  int *fb = (int *)(dst + sl.fb), *gb = (int *)(dst + sl.gb);
+  for (int j = lane; j <= P.n_ops; j += 32) { fb[j] = w.fbase[j]; gb[j] = w.gbase[j]; }
+  double *qc = (double *)(dst + sl.qc);
+  for (int q = lane; q < P.n_queues; q += 32) qc[q] = w.qclock[q];
+  REnt *rs = (REnt *)(dst + sl.rs);
+  for (int j = lane; j < n; j += 32) rs[j] = w.rs[j];
+  int nc = full ? 2 * st.Tf + st.G : st.Tf;
+  double *rd = (double *)(dst + sl.rd);
+  unsigned short *ar = (unsigned short *)(dst + sl.ar);
+  for (int s = lane; s < nc; s += 32) {
+    rd[s] = st.ready[s];
+    ar[s] = (unsigned short)(dc->indeg[s] - st.rem[s]);
+  }
+}
+
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
+  constexpr bool SNAP = (M & SIM_SNAP) != 0;      // delta evaluation: snapshots, first rounds, resume
   // mode known at compile time in the specialised variants (forward mode then
   // drops every backward / ring path)
   constexpr int MODE = (M & SIM_FULL) ? 1 : (M & SIM_FWD) ? 0 : -1;
@@ -853,6 +992,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     }
     st.rem[s] = (unsigned short)indeg;
     st.ready[s] = 0.0;
+    if (SNAP) w.dc->indeg[s] = (unsigned short)indeg;
     if (FULL) {
       int outd = 1;
       for (int i = T.op_out_off[o]; i < T.op_out_off[o + 1]; ++i) {
@@ -861,6 +1001,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       st.rem[Tf + s] = (unsigned short)outd;
       st.ready[Tf + s] = 0.0;
+      if (SNAP) w.dc->indeg[Tf + s] = (unsigned short)outd;
       int pm = T.op_param_mask[o];
       if (pm >= 0) {
         int g = w.gmap[o];
@@ -871,6 +1012,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           int c = 2 * Tf + w.gbase[o] + k;
           st.rem[c] = (unsigned short)(P.map_size[g] / P.map_ngroups[g]);
           st.ready[c] = 0.0;
+          if (SNAP) w.dc->indeg[c] = (unsigned short)(P.map_size[g] / P.map_ngroups[g]);
         }
       }
     }
@@ -878,24 +1020,76 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   __syncwarp();
   int n = 0;
   bool okc = true;
-  for (int base = 0; base < Tf; base += 32) {
-    int s = base + lane;
-    bool want = false;
-    unsigned long long key = 0;
-    int q = 0;
-    double exe = 0.0;
-    if (s < Tf && st.rem[s] == 0) {
+  int round = 0, next_snap = 0x7fffffff;  // (SNAP) round counter, round of the next snapshot
+  if (SNAP && w.dc->restore) {
+    // resume: counters = new in-degrees minus the arrivals recorded at the
+    // snapshot (the changed op's own counters start fresh), clocks, ready set
+    const char *src = w.dc->restore;
+    const SnapLay sl = snap_layout(P);
+    const SnapHdr *hd = (const SnapHdr *)src;
+    const int Tfo = hd->Tf, chg = w.dc->op;
+    const int *fbo = (const int *)(src + sl.fb), *gbo = (const int *)(src + sl.gb);
+    const double *rdo = (const double *)(src + sl.rd);
+    const unsigned short *aro = (const unsigned short *)(src + sl.ar);
+    for (int s = lane; s < Tf; s += 32) {
       int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
-      key = pack_key(KIND_OP, o, 0, s - w.fbase[o], 0);
-      op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe, SIMPLE);
-      want = true;
+      int k = s - w.fbase[o];
+      int ob = fbo[o];
+      if (o != chg && k < fbo[o + 1] - ob) {  // (an op resized since the snapshot had no arrivals then)
+        st.rem[s] -= aro[ob + k];
+        st.ready[s] = rdo[ob + k];
+        if (FULL) {
+          st.rem[Tf + s] -= aro[Tfo + ob + k];
+          st.ready[Tf + s] = rdo[Tfo + ob + k];
+        }
+      }
     }
-    okc &= push2(want, 0.0, key, exe, q, n, P, w, lane);
+    if (FULL)
+      for (int gi = lane; gi < st.G; gi += 32) {
+        int o = upper_bound(w.gbase, P.n_ops + 1, gi) - 1;
+        int si = gi - w.gbase[o];
+        int ob = gbo[o];
+        if (o != chg && si < gbo[o + 1] - ob) {
+          st.rem[2 * Tf + gi] -= aro[2 * Tfo + ob + si];
+          st.ready[2 * Tf + gi] = rdo[2 * Tfo + ob + si];
+        }
+      }
+    const double *qco = (const double *)(src + sl.qc);
+    for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = qco[q];
+    n = hd->n;
+    const REnt *rso = (const REnt *)(src + sl.rs);
+    for (int i = lane; i < n; i += 32) w.rs[i] = rso[i];
+    if (lane == 0) out.makespan = hd->makespan;
+    round = hd->round;
+    __syncwarp();
+  } else {
+    for (int base = 0; base < Tf; base += 32) {
+      int s = base + lane;
+      bool want = false;
+      unsigned long long key = 0;
+      int q = 0;
+      double exe = 0.0;
+      if (s < Tf && st.rem[s] == 0) {
+        int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
+        key = pack_key(KIND_OP, o, 0, s - w.fbase[o], 0);
+        op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe, SIMPLE);
+        want = true;
+      }
+      okc &= push2(want, 0.0, key, exe, q, n, P, w, lane);
+    }
+  }
+  if (SNAP) {
+    if (w.dc->snap && w.dc->restore_idx + 1 < w.dc->nsnap) next_snap = (w.dc->restore_idx + 1) * w.dc->stride;
+    if (lane == 0) { w.dc->last = w.dc->restore_idx; w.dc->bad = 0; }
   }
   __syncwarp();
   PH_ADD(1, t_init);
   if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
   while (n > 0) {
+    if (SNAP && round == next_snap) {
+      snap_write(P, w, st, n, round, round / w.dc->stride, out.makespan, FULL, lane);
+      next_snap = round / w.dc->stride + 1 < w.dc->nsnap ? round + w.dc->stride : 0x7fffffff;
+    }
     PH_T(t_sel);
     TC(0);
     PH_CNT(11, 1);
@@ -1117,6 +1311,11 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         end = start + myexe;
         w.qclock[myq] = end;
       }
+    }
+    if (SNAP && mine) {
+      unsigned kd = key_kind(mykey);
+      if (kd == KIND_OP) atomicMin(&w.dc->frnd[key_a(mykey)], round);
+      else if (kd == KIND_OP_BWD) atomicMin(&w.dc->brnd[key_a(mykey)], round);
     }
     if (mine) {
       if (end > out.makespan) out.makespan = end;
@@ -1343,8 +1542,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 #ifdef PS_TCYC
     ++tc_r;
 #endif
+    if (SNAP) ++round;
     // (no barrier here: every path above ends with one after its last shared store)
   }
+  if (SNAP && lane == 0) w.dc->rounds = round;
   // makespan: max over lanes
   unsigned long long mb = (unsigned long long)__double_as_longlong(out.makespan);
   unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
@@ -1574,11 +1775,88 @@ struct WarpRng {
   }
 };
 
+// Per-chain delta buffers of an MCMC handle (global memory)
+struct DeltaBufs {
+  ChainDelta *cd;          // [n]
+  char *snaps;             // [n][nsnap][2] snapshot slots
+  int *frb;                // [n][2 copies][forward, backward][n_ops] first rounds
+  unsigned short *indeg;   // [n][snap_counters]
+  unsigned long long snap_bytes;
+  int nsnap;
+};
+
+// Resume point of a proposal that changes op o:
+// R_o = the first round in which a task with an o-dependent successor list ran
+// -- a forward task of o or of one of its producers, or (full-iteration) a
+// backward task of o or of one of its consumers; a source op resumes nowhere.
+// Returns the last usable snapshot index at or before R_o (0: from scratch) and
+// points the warp's delta context at it.
+__device__ inline int delta_prepare(const DevProb &P, const Tab &T, const W2 &w, const DeltaBufs &db, int chain,
+                                    int o, double cost, bool full, bool from_scratch, int lane) {
+  DeltaCtx *dc = w.dc;
+  const ChainDelta ch = dc->ch;
+  int *fb0 = db.frb + (size_t)chain * 4 * P.n_ops;
+  const int *fcur = fb0 + (size_t)(ch.fsel * 2) * P.n_ops, *bcur = fcur + P.n_ops;
+  int *fnew = fb0 + (size_t)((ch.fsel ^ 1) * 2) * P.n_ops, *bnew = fnew + P.n_ops;
+  int j = 0;
+  if (!from_scratch && ch.stride > 0 && ch.nvalid > 1 && P.min_exe > __dmul_rn(cost, 0x1p-50)) {
+    int i0 = T.op_in_off[o], i1 = T.op_in_off[o + 1];
+    int R = i0 == i1 ? 0 : fcur[o];
+    if (full) R = min(R, bcur[o]);
+    for (int i = i0 + lane; i < i1; i += 32) R = min(R, fcur[T.pair_src[T.op_in_pairs[i]]]);
+    if (full)
+      for (int i = T.op_out_off[o] + lane; i < T.op_out_off[o + 1]; i += 32)
+        R = min(R, bcur[T.pair_dst[T.op_out_pairs[i]]]);
+    R = __reduce_min_sync(FULLMASK, R);
+    j = min(R / ch.stride, ch.nvalid - 1);
+    while (j > 0 && ((ch.bad >> j) & 1u)) --j;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    dc->snap = ch.stride > 0 ? db.snaps + (size_t)chain * 2 * db.nsnap * db.snap_bytes : nullptr;
+    dc->restore = j > 0 ? dc->snap + (2ull * j + ((ch.cur >> j) & 1u)) * db.snap_bytes : nullptr;
+    dc->frnd = fnew; dc->brnd = bnew;
+    dc->fsrc = fcur; dc->bsrc = bcur;
+    dc->indeg = db.indeg + (size_t)chain * snap_counters(P);
+    dc->snap_bytes = db.snap_bytes;
+    dc->stride = ch.stride;
+    dc->nsnap = db.nsnap;
+    dc->out_sel = ~ch.cur;
+    dc->op = o;
+    dc->restore_idx = j;
+    dc->r0 = j * ch.stride;
+  }
+  __syncwarp();
+  return j;
+}
+
+// After an accepted delta simulation: its snapshots past the resume point and
+// its first rounds become the chain's current ones.
+__device__ inline void delta_commit(DeltaCtx *dc, int j, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    ChainDelta &ch = dc->ch;
+    if (ch.stride > 0) {
+      int last = dc->last;
+      unsigned upto = last >= 31 ? 0xffffffffu : ((1u << (last + 1)) - 1u);
+      unsigned mask = upto & ~((1u << (j + 1)) - 1u);
+      ch.cur ^= mask;
+      ch.bad = (ch.bad & ~mask) | (dc->bad & mask);
+      ch.nvalid = last + 1;
+    }
+    ch.fsel ^= 1;
+  }
+  __syncwarp();
+}
+
 template <int S>
 __global__ void __launch_bounds__(256, 1)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
-       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns) {
+       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
+       DeltaBufs db) {
+  constexpr bool DELTA = (S & SIM_SNAP) != 0;
+  constexpr bool FULLM = (S & SIM_FULL) != 0;
   extern __shared__ __align__(16) char smem[];
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   int chain = blockIdx.x * wpb + wib;
@@ -1595,6 +1873,10 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   unsigned char *gasg = asgs + (size_t)chain * P.n_slots;
   ChainState cs = st[chain];
   if (cs.status != PS_STATUS_OK) return;
+  if (DELTA) {
+    if (lane == 0) w.dc->ch = db.cd[chain];
+    __syncwarp();
+  }
   for (int i = lane; i < P.n_ops; i += 32) w.mapl[i] = gmapl[i];
   if (lay.asg_global) w.asg = gasg;
   else
@@ -1656,16 +1938,44 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
       __syncwarp();
     }
     double cand;
+    int dj = 0;  // resumed snapshot index of this proposal's delta simulation
     if (same) {
       cand = cs.cost;
     } else {
-      SimOut so = simulate_any<S>(P, T, w, lay, gs, lane);
+      SimOut so;
+      // the initial scoring of a delta chain runs twice: once to learn the
+      // round count (the snapshot spacing), once to take its snapshots
+      const int npass = (DELTA && it < 0) ? 2 : 1;
+#pragma unroll 1
+      for (int pass = 0; pass < npass; ++pass) {
+        if (DELTA) {
+          const bool full = (S & SIM_FULL) ? true : (S & SIM_FWD) ? false : P.full != 0;
+          dj = delta_prepare(P, T, w, db, chain, o, cs.cost, full, it < 0, lane);
+        }
+        so = simulate_any<S>(P, T, w, lay, gs, lane);
+        if (so.status != PS_STATUS_OK) break;
+        if (DELTA) {
+          if (lane == 0) {
+            ChainDelta &ch = w.dc->ch;
+            if (it < 0 && pass == 0) {
+              int r = w.dc->rounds;
+              ch.stride = max(4, (r + db.nsnap - 1) / db.nsnap);
+            } else {
+              ch.rounds_reused += w.dc->r0;
+              ch.rounds_run += w.dc->rounds - w.dc->r0;
+            }
+          }
+          __syncwarp();
+          if (it < 0) delta_commit(w.dc, 0, lane);
+        }
+      }
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
         if (it < 0) {
           cs.started = 1;
           cs.initial = cs.best = cs.cost = __longlong_as_double(0x7ff0000000000000ll);
           if (lane == 0) st[chain] = cs;
+          if (DELTA && lane == 0) db.cd[chain] = w.dc->ch;
           return;
         }
         break;
@@ -1703,6 +2013,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     if (ok) {
       cs.cost = cand;
       cs.accepted++;
+      if (DELTA && !same) delta_commit(w.dc, dj, lane);
     } else {
       for (int i = lane; i < old_size; i += 32) w.asg[base + i] = w.oldasg[i];
       if (lane == 0) w.mapl[o] = old_m;
@@ -1723,6 +2034,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   cs.bpos = rng.bpos;
   cs.mti = rng.mti;
   if (lane == 0) st[chain] = cs;
+  if (DELTA && lane == 0) db.cd[chain] = w.dc->ch;
 }
 
 __global__ void k_best(const ChainState *st, int n, double *best_cost, int *best_chain) {
@@ -1813,6 +2125,7 @@ struct ps_mcmc {
   double *d_best;
   int *d_bestc;
   int cap_n;  // chains the buffers above were sized for
+  DeltaBufs db;  // delta-evaluation state (db.cd == nullptr: every proposal simulates from scratch)
 };
 
 static int ensure_io(ps_problem *pr, size_t n) {
@@ -1934,6 +2247,27 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
       l16[i] = (short)(li < 0 ? -1 : (P.n_cls ? (li | cls[li] << 14) : li));
     }
     if ((rc = upload(ow, l16.data(), l16.size(), &P.link16)) != PS_OK) return rc;
+  }
+  {
+    // delta evaluation: dense ring-counter bound, and a lower bound of every
+    // task time (op tasks from the tables; transfers >= 1 byte; ring hops
+    // >= the smallest shard over 64 devices)
+    P.n_rings = 0;
+    double mn = INFINITY, min_shard = INFINITY;
+    for (int o = 0; o < P.n_ops; ++o) {
+      int mg = 0;
+      for (int g = d->op_map_off[o]; g < d->op_map_off[o + 1]; ++g) {
+        mg = std::max(mg, d->map_ngroups[g]);
+        if (d->op_param_mask[o] >= 0 && d->map_shard[g] < min_shard) min_shard = d->map_shard[g];
+      }
+      if (d->op_param_mask[o] >= 0) P.n_rings += mg;
+    }
+    for (int i = 0; i < P.n_maps * P.n_kinds; ++i) mn = std::min(mn, std::min(d->exe_fwd[i], d->exe_bwd[i]));
+    for (int l = 0; l < P.n_links; ++l) {
+      mn = std::min(mn, d->link_lat[l] + 1.0 / d->link_bw[l]);
+      if (min_shard < INFINITY) mn = std::min(mn, d->link_lat[l] + (min_shard / 64.0) / d->link_bw[l]);
+    }
+    P.min_exe = (mn > 0.0 && mn < INFINITY) ? mn : 0.0;
   }
   // ---- overlap tables: count rows -> scan -> fill, then the column index
   int *cnt = nullptr, *off = nullptr, *ccnt = nullptr, *coff = nullptr;
@@ -2064,6 +2398,9 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
   CK(cudaFuncSetAttribute(k_mcmc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<SIM_SNAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch<0>, pr->wpb * 32, pr->smem_per_block));
@@ -2346,6 +2683,27 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     CK(cudaMalloc(&m->trace_cand, (size_t)n * params->trace_capacity * sizeof(double)));
     CK(cudaMalloc(&m->trace_ok, (size_t)n * params->trace_capacity));
   }
+  {
+    // delta evaluation: snapshots per chain (two copies per index), first
+    // rounds, in-degrees.  Off when some task can take zero time, when asked
+    // (params->delta == 0 / PS_NO_DELTA), or when fewer than 4 snapshot indices
+    // fit in a quarter of the free device memory (8 GiB at most).
+    size_t sb = snap_layout(P).total;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    size_t budget = std::min((size_t)8 << 30, free_b / 4);
+    int ns = (int)std::min<size_t>(24, budget / ((size_t)n * 2 * sb));
+    bool on = params->delta != 0 && P.min_exe > 0.0 && ns >= 4 && !getenv("PS_NO_DELTA");
+    if (on) {
+      m->db.nsnap = ns;
+      m->db.snap_bytes = sb;
+      CK(cudaMalloc(&m->db.cd, (size_t)n * sizeof(ChainDelta)));
+      CK(cudaMemset(m->db.cd, 0, (size_t)n * sizeof(ChainDelta)));
+      CK(cudaMalloc(&m->db.snaps, (size_t)n * 2 * ns * sb));
+      CK(cudaMalloc(&m->db.frb, (size_t)n * 4 * P.n_ops * sizeof(int)));
+      CK(cudaMalloc(&m->db.indeg, (size_t)n * snap_counters(P) * sizeof(unsigned short)));
+    }
+  }
   *out = m;
   return PS_OK;
 }
@@ -2357,11 +2715,14 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   int wpb = pr->wpb;
   int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
-  auto km = !pr->simple ? k_mcmc<0> : pr->P.full ? k_mcmc<SIM_SIMPLE | SIM_FULL> : k_mcmc<SIM_SIMPLE | SIM_FWD>;
+  auto km = m->db.cd ? (!pr->simple ? k_mcmc<SIM_SNAP>
+                                     : pr->P.full ? k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FULL>
+                                                  : k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FWD>)
+                    : (!pr->simple ? k_mcmc<0> : pr->P.full ? k_mcmc<SIM_SIMPLE | SIM_FULL> : k_mcmc<SIM_SIMPLE | SIM_FWD>);
   km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
-      m->params.record_trace ? m->params.trace_capacity : 0, m->scratch, budget_ns);
+      m->params.record_trace ? m->params.trace_capacity : 0, m->scratch, budget_ns, m->db);
   CK(cudaGetLastError());
   return PS_OK;
 }
@@ -2385,6 +2746,15 @@ int ps_mcmc_read(ps_mcmc *m, ps_chain_summary *summary, int32_t *best_map, uint8
       s.initial_cost = st[i].initial; s.best_cost = st[i].best; s.cost = st[i].cost; s.beta = st[i].beta;
       s.proposals = st[i].proposals; s.accepted = st[i].accepted; s.status = st[i].status;
       s.err_a = st[i].err_a; s.err_b = st[i].err_b; s.last_op = st[i].last_op;
+      s.rounds_run = s.rounds_reused = 0;
+    }
+    if (m->db.cd) {
+      std::vector<ChainDelta> cd(m->n);
+      CK(cudaMemcpy(cd.data(), m->db.cd, (size_t)m->n * sizeof(ChainDelta), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < m->n; ++i) {
+        summary[i].rounds_run = cd[i].rounds_run;
+        summary[i].rounds_reused = cd[i].rounds_reused;
+      }
     }
   }
   if (best_map) CK(cudaMemcpy(best_map, m->best_maps, (size_t)m->n * pr->P.n_ops * sizeof(int), cudaMemcpyDeviceToHost));
@@ -2473,6 +2843,7 @@ void ps_mcmc_destroy(ps_mcmc *m) {
     cudaFree(m->d_best); cudaFree(m->d_bestc);
   }
   cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok);
+  cudaFree(m->db.cd); cudaFree(m->db.snaps); cudaFree(m->db.frb); cudaFree(m->db.indeg);
   if (m->scratch) {  // keep the largest chain scratch for the problem's next handle
     if (m->scratch_bytes >= m->prob->mcmc_scratch_bytes) {
       cudaFree(m->prob->mcmc_scratch);

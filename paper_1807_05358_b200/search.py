@@ -68,6 +68,7 @@ class SearchParams:
     rng: str = RNG_MT19937          # "mt19937" replays the reference; "philox" = shared Philox stream
     segment: int = 256              # proposals per kernel launch between host checks
     device: int = 0
+    delta: bool = True              # checkpointed delta evaluation of proposals (same results; faster)
 
 
 @dataclass
@@ -299,7 +300,7 @@ def _run_chains(low, params, initial, live, summaries, traces, best, start_err) 
     # fixed-length search, or one segment of a time-boxed one (read after each)
     record = cap if deterministic else seg
     mp = nat.PsMcmcParams(rng_mode, params.beta is not None, float(params.beta or 0.0), math.log(10.0),
-                          1 if record else 0, record)
+                          1 if record else 0, record, 1 if params.delta else 0)
     h = ctypes.c_void_p()
     nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), n, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds_u64),
                                nat.ptr(mt) if mt is not None else None, ctypes.byref(h)), "ps_mcmc_create")

@@ -135,3 +135,43 @@ def test_criterion_1_delta_equals_a_fresh_build_on_10000_changes(oracle):
         assert got == [float(x) for x in fresh], scenario
         assert got == [float(x) for x in oracle.makespans(g, topo, prof, mode, seen)], scenario
         scenario += 1
+
+
+def test_random10k_mcmc_matches_oracle(oracle):
+    """The 10k-op random DAG (BASELINE config 5; every per-chain table in global
+    memory): a short MCMC in both modes, chain summaries against the oracle."""
+    g = ps.random_dag(10000, seed=1000)
+    topo = ps.multi_node_topology(4, 4)
+    prof = ps.CostProfile()
+    init = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, 4, [1, 2, 3])
+    for mode in (ps.MODE_FULL, ps.MODE_FORWARD):
+        rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=12, seed=5, max_degree=4, mode=mode,
+                                                            initial=init, polish=False, rng="philox"))
+        ref = oracle.mcmc(g, topo, prof, mode, init, [5 + 1000003 * c for c in range(4)], 12, 4,
+                          rng_mode="philox", threads=4)
+        for ci, ch in enumerate(rep.chains):
+            assert (ch.initial_cost, ch.best_cost, ch.proposals, ch.accepted, ch.beta) == tuple(ref["summary"][ci][:5])
+
+
+def test_time_boxed_search_records_its_trace_and_verifies():
+    """budget_seconds mode: every proposal lands in the report's trace (read back
+    segment by segment) and check_interval re-verifies the chains."""
+    g = ps.alexnet_like()
+    topo = ps.single_node_topology(4)
+    prof = ps.CostProfile()
+    rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(budget_seconds=0.5, seed=1, max_degree=4, polish=False,
+                                                        segment=64, check_interval=32, mode=ps.MODE_FULL))
+    assert rep.proposals > 0 and len(rep.trace) == rep.proposals
+    assert [i for i, _, _ in rep.trace] == list(range(1, rep.proposals + 1))
+    for c in rep.chains:
+        assert c.termination in ("budget", "stagnation")
+    # the trace is the chains' own: replaying chain 0's count deterministically gives the same prefix
+    n0 = rep.chains[0].proposals
+    det = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=n0, seed=1, max_degree=4, polish=False,
+                                                        mode=ps.MODE_FULL, initial=[ps.data_parallel_strategy(g, topo)]))
+    assert [(c, a) for _, c, a in rep.trace[:n0]] == [(c, a) for _, c, a in det.trace]
+    # a proposal cap with a budget stops at the cap
+    capped = ps.mcmc_search(g, topo, prof, ps.SearchParams(budget_seconds=30.0, max_proposals=100, seed=2,
+                                                           max_degree=4, polish=False, segment=48))
+    assert all(c.proposals == 100 and c.termination == "proposal-limit" for c in capped.chains)
+    assert len(capped.trace) == 200

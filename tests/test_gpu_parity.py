@@ -443,3 +443,78 @@ def test_time_boxed_segments_are_exact_prefixes(oracle):
         for j, c in enumerate(idx):
             s = summ[c]
             assert (s.initial_cost, s.best_cost, s.proposals, s.accepted) == tuple(ref["summary"][j][:4]), (c, p)
+
+
+def _run_mcmc_raw(low, init, seeds, proposals, delta, record=0):
+    import ctypes
+    from paper_1807_05358_b200 import _native as nat
+    C = len(init)
+    maps = np.zeros((C, low.n_ops), dtype=np.int32)
+    asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+    for i, s in enumerate(init):
+        low.encode(s, maps[i], asg[i])
+    L = nat.lib()
+    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 1 if record else 0, record, delta)
+    h = ctypes.c_void_p()
+    sd = np.array(seeds, dtype=np.uint64)
+    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(sd), None,
+                               ctypes.byref(h)), "ps_mcmc_create")
+    try:
+        for _ in range(0, proposals, 50):
+            nat.check(L.ps_mcmc_run(h, min(50, proposals), None), "ps_mcmc_run")
+        summ = (nat.PsChainSummary * C)()
+        bm = np.zeros((C, low.n_ops), dtype=np.int32)
+        ba = np.zeros((C, low.n_slots), dtype=np.uint8)
+        tc = np.zeros((C, max(record, 1)))
+        nat.check(L.ps_mcmc_read(h, summ, nat.ptr(bm), nat.ptr(ba), nat.ptr(tc) if record else None, None),
+                  "ps_mcmc_read")
+    finally:
+        L.ps_mcmc_destroy(h)
+    return summ, bm, ba, tc
+
+
+@pytest.mark.parametrize("mode", [ps.MODE_FULL, ps.MODE_FORWARD])
+def test_delta_evaluation_equals_from_scratch_and_oracle(oracle, mode):
+    """Checkpointed delta evaluation (resume from the last snapshot before the
+    changed op's first dependent round) gives the same trajectories, best
+    strategies and trace as re-simulating every proposal from time zero, and
+    the oracle's; and it does skip rounds."""
+    from paper_1807_05358_b200.lowering import lower
+    g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
+    prof = ps.CostProfile()
+    C, P = 96, 150
+    init = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, md, list(range(1, C)))
+    seeds = [1000003 * c for c in range(C)]
+    low = lower(g, topo, prof, mode, max_degree=md, strategies=init)
+    a, am, aa, at = _run_mcmc_raw(low, init, seeds, P, 1, record=P)
+    b, bm, ba, bt = _run_mcmc_raw(low, init, seeds, P, 0, record=P)
+    key = lambda s: (s.initial_cost, s.best_cost, s.cost, s.proposals, s.accepted, s.beta, s.status)
+    assert [key(s) for s in a] == [key(s) for s in b]
+    assert np.array_equal(am, bm) and np.array_equal(aa, ba) and np.array_equal(at, bt)
+    reused = sum(s.rounds_reused for s in a)
+    run = sum(s.rounds_run for s in a)
+    assert reused > 0.05 * (reused + run), (reused, run)
+    assert all(s.rounds_reused == 0 for s in b)
+    ref = oracle.mcmc(g, topo, prof, mode, init[:16], seeds[:16], P, md, rng_mode="philox", threads=8)
+    assert [key(s)[:2] + key(s)[3:5] for s in a[:16]] == [(r[0], r[1], r[2], r[3]) for r in ref["summary"]]
+    assert np.array_equal(at[:16], ref["cand"])
+
+
+def test_delta_evaluation_on_large_and_heterogeneous_problems(oracle):
+    """Delta evaluation where the counters live in global memory (ResNet-101 on
+    64 devices), with capacity reruns, and on a heterogeneous topology."""
+    from paper_1807_05358_b200.lowering import lower
+    rng = random.Random(5)
+    cases = [(ps.resnet101(), ps.multi_node_topology(16, 4), 8, ps.CostProfile(), 24, 40),
+             (ps.random_dag(40, seed=77), _hetero_topology(rng),
+              4, ps.CostProfile(fallback=ps.AnalyticCostModel(throughput={"tpu": 3e12})), 32, 120)]
+    for g, topo, md, prof, C, P in cases:
+        for mode in (ps.MODE_FULL, ps.MODE_FORWARD):
+            init = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, md, list(range(1, C)))
+            seeds = [7 + 1000003 * c for c in range(C)]
+            low = lower(g, topo, prof, mode, max_degree=md, strategies=init, ready_capacity=16)
+            a, am, aa, at = _run_mcmc_raw(low, init, seeds, P, 1, record=P)
+            ref = oracle.mcmc(g, topo, prof, mode, init, seeds, P, md, rng_mode="philox", threads=8)
+            assert [(s.initial_cost, s.best_cost, s.proposals, s.accepted) for s in a] == \
+                [tuple(r[:4]) for r in ref["summary"]], mode
+            assert np.array_equal(at, ref["cand"])
