@@ -380,12 +380,20 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15
 // an accepted proposal keeps the snapshots before its resume point and replaces
 // the ones after it.
 struct __align__(16) SnapHdr {
-  int round, n, Tf, G;
+  int round, n, nlist, valid;
   double makespan;
-  int valid, pad_[9];
+  int pad_[10];
 };
 
-struct SnapLay { size_t fb, gb, qc, rs, rd, ar, total; };
+// A counter recorded in a snapshot: (op | kind << 16 | k << 18), arrivals, ready
+// time; kind 0 forward task, 1 backward task, 2 ring (k = shard).  Only counters
+// that some arrival has touched and that may still be read are recorded: tasks
+// still waiting on predecessors, and rings (their slot keeps the per-hop bytes
+// once hop 0 is out).  A task that ran or is in the ready set is never counted
+// again, so its counter can restart from its in-degree.
+struct __align__(16) SnapEnt { unsigned code, arr; double ready; };
+
+struct SnapLay { size_t qc, rs, ls, total; int lcap; };
 
 __host__ __device__ inline size_t snap_counters(const DevProb &P) {
   return P.full ? 2 * (size_t)P.n_slots + (size_t)P.n_rings : (size_t)P.n_slots;
@@ -394,12 +402,10 @@ __host__ __device__ inline size_t snap_counters(const DevProb &P) {
 __host__ __device__ inline SnapLay snap_layout(const DevProb &P) {
   SnapLay L;
   size_t o = sizeof(SnapHdr);
-  L.fb = o; o += al16(4 * (size_t)(P.n_ops + 1));
-  L.gb = o; o += al16(4 * (size_t)(P.n_ops + 1));
   L.qc = o; o += al16(8 * (size_t)P.n_queues);
   L.rs = o; o += al16(32 * (size_t)P.cap);
-  L.rd = o; o += al16(8 * snap_counters(P));
-  L.ar = o; o += al16(2 * snap_counters(P));
+  L.lcap = (int)(snap_counters(P) < 2048 ? snap_counters(P) : 2048);
+  L.ls = o; o += sizeof(SnapEnt) * (size_t)L.lcap;
   L.total = al16(o);
   return L;
 }
@@ -898,42 +904,59 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
 }
 
 // Snapshot of the simulation state at the start of round `round` (index i):
-// queue clocks, ready set, running makespan, and per dense counter its ready
-// time and arrivals so far (in-degree minus remaining), with the dense layout
-// (fbase / gbase) they are indexed by.  A ready set larger than the resume
-// capacity marks the index unusable.
-__device__ __noinline__ void snap_write(const DevProb &P, const W2 &w, const State &st, int n, int round, int i,
-                                        double mk, bool full, int lane) {
+// queue clocks, ready set, running makespan, and the touched counters (SnapEnt).
+// A ready set or counter list larger than the snapshot holds marks the index
+// unusable.
+__device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const State &st, int n, int round, int i,
+                                           double mk, bool full, int lane) {
   DeltaCtx *dc = w.dc;
   const SnapLay sl = snap_layout(P);
   char *dst = dc->snap + (2ull * (unsigned)i + ((dc->out_sel >> i) & 1u)) * dc->snap_bytes;
+  SnapEnt *ls = (SnapEnt *)(dst + sl.ls);
+  const int Tf = st.Tf, nc = full ? 2 * Tf + st.G : Tf;
+  int nl = 0;
+  bool ok = n <= P.cap;
+  for (int base = 0; base < nc && ok; base += 32) {
+    int s = base + lane;
+    bool rec = false;
+    unsigned rem = 0;
+    double rd = 0.0;
+    if (s < nc) {
+      rem = st.rem[s];
+      rd = st.ready[s];
+      rec = rd > 0.0 && (rem > 0 || s >= 2 * Tf);
+    }
+    unsigned bm = __ballot_sync(FULLMASK, rec);
+    if (nl + __popc(bm) > sl.lcap) { ok = false; break; }
+    if (rec) {
+      int kind = s < Tf ? 0 : s < 2 * Tf ? 1 : 2;
+      int x = kind == 0 ? s : kind == 1 ? s - Tf : s - 2 * Tf;
+      const int *bs = kind == 2 ? w.gbase : w.fbase;
+      int o = upper_bound(bs, P.n_ops + 1, x) - 1;
+      SnapEnt e;
+      e.code = (unsigned)o | (unsigned)kind << 16 | (unsigned)(x - bs[o]) << 18;
+      e.arr = (unsigned)dc->indeg[s] - rem;
+      e.ready = rd;
+      ls[nl + __popc(bm & ((1u << lane) - 1u))] = e;
+    }
+    nl += __popc(bm);
+  }
   unsigned long long mb = (unsigned long long)__double_as_longlong(mk);
   unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
   unsigned lo = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32) == hi ? (unsigned)mb : 0u);
-  bool ok = n <= P.cap;
   if (lane == 0) {
     SnapHdr h;
-    h.round = round; h.n = n; h.Tf = st.Tf; h.G = st.G;
+    h.round = round; h.n = n; h.nlist = nl; h.valid = ok;
     h.makespan = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
-    h.valid = ok;
     *(SnapHdr *)dst = h;
     dc->last = i;
     if (!ok) dc->bad |= 1u << i;
   }
   if (!ok) return;
-  int *fb = (int *)(dst + sl.fb), *gb = (int *)(dst + sl.gb);
-  for (int j = lane; j <= P.n_ops; j += 32) { fb[j] = w.fbase[j]; gb[j] = w.gbase[j]; }
   double *qc = (double *)(dst + sl.qc);
   for (int q = lane; q < P.n_queues; q += 32) qc[q] = w.qclock[q];
   REnt *rs = (REnt *)(dst + sl.rs);
   for (int j = lane; j < n; j += 32) rs[j] = w.rs[j];
-  int nc = full ? 2 * st.Tf + st.G : st.Tf;
-  double *rd = (double *)(dst + sl.rd);
-  unsigned short *ar = (unsigned short *)(dst + sl.ar);
-  for (int s = lane; s < nc; s += 32) {
-    rd[s] = st.ready[s];
-    ar[s] = (unsigned short)(dc->indeg[s] - st.rem[s]);
-  }
 }
 
 template <int M>
@@ -1022,38 +1045,24 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   bool okc = true;
   int round = 0, next_snap = 0x7fffffff;  // (SNAP) round counter, round of the next snapshot
   if (SNAP && w.dc->restore) {
-    // resume: counters = new in-degrees minus the arrivals recorded at the
-    // snapshot (the changed op's own counters start fresh), clocks, ready set
+    // resume: recorded counters = new in-degree minus the arrivals recorded at
+    // the snapshot (the changed op's own counters start fresh; a counter of an op
+    // resized since the snapshot had no arrivals then), clocks, ready set
     const char *src = w.dc->restore;
     const SnapLay sl = snap_layout(P);
     const SnapHdr *hd = (const SnapHdr *)src;
-    const int Tfo = hd->Tf, chg = w.dc->op;
-    const int *fbo = (const int *)(src + sl.fb), *gbo = (const int *)(src + sl.gb);
-    const double *rdo = (const double *)(src + sl.rd);
-    const unsigned short *aro = (const unsigned short *)(src + sl.ar);
-    for (int s = lane; s < Tf; s += 32) {
-      int o = upper_bound(w.fbase, P.n_ops + 1, s) - 1;
-      int k = s - w.fbase[o];
-      int ob = fbo[o];
-      if (o != chg && k < fbo[o + 1] - ob) {  // (an op resized since the snapshot had no arrivals then)
-        st.rem[s] -= aro[ob + k];
-        st.ready[s] = rdo[ob + k];
-        if (FULL) {
-          st.rem[Tf + s] -= aro[Tfo + ob + k];
-          st.ready[Tf + s] = rdo[Tfo + ob + k];
-        }
-      }
+    const int chg = w.dc->op, nl = hd->nlist;
+    const SnapEnt *ls = (const SnapEnt *)(src + sl.ls);
+    for (int e = lane; e < nl; e += 32) {
+      SnapEnt en = ls[e];
+      int o = en.code & 0xffff, kind = (en.code >> 16) & 3, k = en.code >> 18;
+      if (o == chg) continue;
+      const int *bs = kind == 2 ? w.gbase : w.fbase;
+      if (k >= bs[o + 1] - bs[o]) continue;
+      int c = (kind == 0 ? 0 : kind == 1 ? Tf : 2 * Tf) + bs[o] + k;
+      st.rem[c] -= (unsigned short)en.arr;
+      st.ready[c] = en.ready;
     }
-    if (FULL)
-      for (int gi = lane; gi < st.G; gi += 32) {
-        int o = upper_bound(w.gbase, P.n_ops + 1, gi) - 1;
-        int si = gi - w.gbase[o];
-        int ob = gbo[o];
-        if (o != chg && si < gbo[o + 1] - ob) {
-          st.rem[2 * Tf + gi] -= aro[2 * Tfo + ob + si];
-          st.ready[2 * Tf + gi] = rdo[2 * Tfo + ob + si];
-        }
-      }
     const double *qco = (const double *)(src + sl.qc);
     for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = qco[q];
     n = hd->n;
@@ -2691,7 +2700,7 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     size_t sb = snap_layout(P).total;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    size_t budget = std::min((size_t)8 << 30, free_b / 4);
+    size_t budget = std::min((size_t)8 << 30, total_b / 16);
     int ns = (int)std::min<size_t>(24, budget / ((size_t)n * 2 * sb));
     bool on = params->delta != 0 && P.min_exe > 0.0 && ns >= 4 && !getenv("PS_NO_DELTA");
     if (on) {

@@ -460,8 +460,8 @@ def _run_mcmc_raw(low, init, seeds, proposals, delta, record=0):
     nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(sd), None,
                                ctypes.byref(h)), "ps_mcmc_create")
     try:
-        for _ in range(0, proposals, 50):
-            nat.check(L.ps_mcmc_run(h, min(50, proposals), None), "ps_mcmc_run")
+        for done in range(0, proposals, 50):
+            nat.check(L.ps_mcmc_run(h, min(50, proposals - done), None), "ps_mcmc_run")
         summ = (nat.PsChainSummary * C)()
         bm = np.zeros((C, low.n_ops), dtype=np.int32)
         ba = np.zeros((C, low.n_slots), dtype=np.uint8)
