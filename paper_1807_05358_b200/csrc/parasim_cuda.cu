@@ -643,7 +643,7 @@ __device__ inline void delta_first_rounds(const DevProb &P, DeltaCtx *dc, int la
   const int *fs = dc->fsrc, *bs = dc->bsrc;
   int *fd = dc->frnd, *bd = dc->brnd;
   for (int i = lane; i < P.n_ops; i += 32) {
-    int a = fs ? fs[i] : 0x7fffffff, b = bs ? bs[i] : 0x7fffffff;
+    int a = fs && r0 > 0 ? fs[i] : 0x7fffffff, b = bs && r0 > 0 ? bs[i] : 0x7fffffff;
     fd[i] = a < r0 ? a : 0x7fffffff;
     bd[i] = b < r0 ? b : 0x7fffffff;
   }
@@ -1817,7 +1817,7 @@ __device__ inline int delta_prepare(const DevProb &P, const Tab &T, const W2 &w,
       for (int i = T.op_out_off[o] + lane; i < T.op_out_off[o + 1]; i += 32)
         R = min(R, bcur[T.pair_dst[T.op_out_pairs[i]]]);
     R = __reduce_min_sync(FULLMASK, R);
-    j = min(R / ch.stride, ch.nvalid - 1);
+    j = max(0, min(R / ch.stride, ch.nvalid - 1));
     while (j > 0 && ((ch.bad >> j) & 1u)) --j;
   }
   __syncwarp();
@@ -2710,6 +2710,7 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
       CK(cudaMemset(m->db.cd, 0, (size_t)n * sizeof(ChainDelta)));
       CK(cudaMalloc(&m->db.snaps, (size_t)n * 2 * ns * sb));
       CK(cudaMalloc(&m->db.frb, (size_t)n * 4 * P.n_ops * sizeof(int)));
+      CK(cudaMemset(m->db.frb, 0x7f, (size_t)n * 4 * P.n_ops * sizeof(int)));  // "never ran"
       CK(cudaMalloc(&m->db.indeg, (size_t)n * snap_counters(P) * sizeof(unsigned short)));
     }
   }
@@ -2789,6 +2790,16 @@ int ps_mcmc_stop(ps_mcmc *m, const uint8_t *stop) {
 
 
 int ps_mcmc_chains(const ps_mcmc *m) { return m ? m->n : 0; }
+
+// debug: raw per-chain delta bookkeeping (stride, nvalid, cur, bad, fsel, pad,
+// rounds_run, rounds_reused) -- 40 bytes per chain; PS_ERR_INVALID when delta is off
+int ps_debug_delta_state(ps_mcmc *m, void *out) {
+  if (!m || !m->db.cd) return fail(PS_ERR_INVALID, "delta evaluation is off for this handle");
+  CK(cudaSetDevice(m->prob->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, m->db.cd, (size_t)m->n * sizeof(ChainDelta), cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
 
 int ps_debug_tcyc(long long *out) {
 #ifdef PS_TCYC
