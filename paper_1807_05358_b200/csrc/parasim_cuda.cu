@@ -380,32 +380,33 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15
 // an accepted proposal keeps the snapshots before its resume point and replaces
 // the ones after it.
 struct __align__(16) SnapHdr {
-  int round, n, nlist, valid;
+  int round, n, Tf, G;
   double makespan;
-  int pad_[10];
+  int valid, epoch;        // epoch: in-degree buffer of the strategy that wrote it
+  int pad_[8];
 };
 
-// A counter recorded in a snapshot: (op | kind << 16 | k << 18), arrivals, ready
-// time; kind 0 forward task, 1 backward task, 2 ring (k = shard).  Only counters
-// that some arrival has touched and that may still be read are recorded: tasks
-// still waiting on predecessors, and rings (their slot keeps the per-hop bytes
-// once hop 0 is out).  A task that ran or is in the ready set is never counted
-// again, so its counter can restart from its in-degree.
-struct __align__(16) SnapEnt { unsigned code, arr; double ready; };
-
-struct SnapLay { size_t qc, rs, ls, total; int lcap; };
+// Snapshot layout: header, dense layout (fbase / gbase), queue clocks, ready set,
+// and the raw dense counters (remaining count, ready time).  Arrivals are
+// in-degree minus remaining, with the in-degrees of the writing strategy kept
+// in a per-chain epoch buffer (written once per simulation, by its init).
+struct SnapLay { size_t fb, gb, qc, rs, rm, rd, total; };
 
 __host__ __device__ inline size_t snap_counters(const DevProb &P) {
   return P.full ? 2 * (size_t)P.n_slots + (size_t)P.n_rings : (size_t)P.n_slots;
 }
 
+__host__ __device__ inline size_t snap_counters_pad(const DevProb &P) { return (snap_counters(P) + 7) & ~(size_t)7; }
+
 __host__ __device__ inline SnapLay snap_layout(const DevProb &P) {
   SnapLay L;
   size_t o = sizeof(SnapHdr);
+  L.fb = o; o += al16(4 * (size_t)(P.n_ops + 1));
+  L.gb = o; o += al16(4 * (size_t)(P.n_ops + 1));
   L.qc = o; o += al16(8 * (size_t)P.n_queues);
   L.rs = o; o += al16(32 * (size_t)P.cap);
-  L.lcap = (int)(snap_counters(P) < 2048 ? snap_counters(P) : 2048);
-  L.ls = o; o += sizeof(SnapEnt) * (size_t)L.lcap;
+  L.rm = o; o += al16(2 * snap_counters_pad(P));
+  L.rd = o; o += al16(8 * snap_counters_pad(P));
   L.total = al16(o);
   return L;
 }
@@ -416,6 +417,7 @@ struct ChainDelta {
   unsigned cur, bad;       // bit i: copy holding index i / index i unusable
   int fsel, pad_;          // which first-round buffer belongs to the current strategy
   long long rounds_run, rounds_reused;
+  unsigned char ep[32];    // in-degree epoch buffer of the snapshot at index i (current copy)
 };
 
 // Per-simulation delta context, in the warp's shared-memory slice.
@@ -423,7 +425,10 @@ struct DeltaCtx {
   char *snap;              // this chain's snapshot slots: index i, copy b at snap + (2 i + b) snap_bytes
   const char *restore;     // snapshot to resume from (null: from time zero)
   int *frnd, *brnd;        // this simulation's first round per op (forward / backward tasks)
-  unsigned short *indeg;   // this simulation's dense counter in-degrees (global)
+  unsigned short *indeg;   // this simulation's dense counter in-degrees (global epoch buffer)
+  const unsigned short *indeg0;  // epoch buffer 0 of the chain (snapshot headers name theirs)
+  unsigned long long ep_stride;  // elements per epoch buffer
+  int epoch;               // this simulation's epoch buffer
   unsigned long long snap_bytes;
   int stride, nsnap;       // rounds between snapshots; snapshot indices per copy
   unsigned out_sel;        // bit i: the copy index i is written to
@@ -903,60 +908,41 @@ __device__ inline double trace_nbytes(const DevProb &P, const Tab &T, const W2 &
   return 0.0;
 }
 
+__device__ __forceinline__ void copy16(void *dst, const void *src, size_t bytes, int lane) {
+  const int4 *s4 = (const int4 *)src;
+  int4 *d4 = (int4 *)dst;
+  int n = (int)((bytes + 15) >> 4);
+  for (int i = lane; i < n; i += 32) d4[i] = s4[i];
+}
+
 // Snapshot of the simulation state at the start of round `round` (index i):
-// queue clocks, ready set, running makespan, and the touched counters (SnapEnt).
-// A ready set or counter list larger than the snapshot holds marks the index
-// unusable.
+// vector copies of the dense layout, queue clocks, ready set and raw counters.
+// A ready set larger than a snapshot holds marks the index unusable.
 __device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const State &st, int n, int round, int i,
                                            double mk, bool full, int lane) {
   DeltaCtx *dc = w.dc;
   const SnapLay sl = snap_layout(P);
   char *dst = dc->snap + (2ull * (unsigned)i + ((dc->out_sel >> i) & 1u)) * dc->snap_bytes;
-  SnapEnt *ls = (SnapEnt *)(dst + sl.ls);
-  const int Tf = st.Tf, nc = full ? 2 * Tf + st.G : Tf;
-  int nl = 0;
+  const int nc = full ? 2 * st.Tf + st.G : st.Tf;
   bool ok = n <= P.cap;
-  for (int base = 0; base < nc && ok; base += 32) {
-    int s = base + lane;
-    bool rec = false;
-    unsigned rem = 0;
-    double rd = 0.0;
-    if (s < nc) {
-      rem = st.rem[s];
-      rd = st.ready[s];
-      rec = rd > 0.0 && (rem > 0 || s >= 2 * Tf);
-    }
-    unsigned bm = __ballot_sync(FULLMASK, rec);
-    if (nl + __popc(bm) > sl.lcap) { ok = false; break; }
-    if (rec) {
-      int kind = s < Tf ? 0 : s < 2 * Tf ? 1 : 2;
-      int x = kind == 0 ? s : kind == 1 ? s - Tf : s - 2 * Tf;
-      const int *bs = kind == 2 ? w.gbase : w.fbase;
-      int o = upper_bound(bs, P.n_ops + 1, x) - 1;
-      SnapEnt e;
-      e.code = (unsigned)o | (unsigned)kind << 16 | (unsigned)(x - bs[o]) << 18;
-      e.arr = (unsigned)dc->indeg[s] - rem;
-      e.ready = rd;
-      ls[nl + __popc(bm & ((1u << lane) - 1u))] = e;
-    }
-    nl += __popc(bm);
-  }
   unsigned long long mb = (unsigned long long)__double_as_longlong(mk);
   unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
   unsigned lo = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32) == hi ? (unsigned)mb : 0u);
   if (lane == 0) {
     SnapHdr h;
-    h.round = round; h.n = n; h.nlist = nl; h.valid = ok;
+    h.round = round; h.n = n; h.Tf = st.Tf; h.G = st.G; h.valid = ok; h.epoch = dc->epoch;
     h.makespan = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
     *(SnapHdr *)dst = h;
     dc->last = i;
     if (!ok) dc->bad |= 1u << i;
   }
   if (!ok) return;
-  double *qc = (double *)(dst + sl.qc);
-  for (int q = lane; q < P.n_queues; q += 32) qc[q] = w.qclock[q];
-  REnt *rs = (REnt *)(dst + sl.rs);
-  for (int j = lane; j < n; j += 32) rs[j] = w.rs[j];
+  copy16(dst + sl.fb, w.fbase, 4 * (size_t)(P.n_ops + 1), lane);
+  if (full) copy16(dst + sl.gb, w.gbase, 4 * (size_t)(P.n_ops + 1), lane);
+  copy16(dst + sl.qc, w.qclock, 8 * (size_t)P.n_queues, lane);
+  copy16(dst + sl.rs, w.rs, 32 * (size_t)n, lane);
+  copy16(dst + sl.rm, st.rem, 2 * (size_t)nc, lane);
+  copy16(dst + sl.rd, st.ready, 8 * (size_t)nc, lane);
 }
 
 template <int M>
@@ -1045,24 +1031,58 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   bool okc = true;
   int round = 0, next_snap = 0x7fffffff;  // (SNAP) round counter, round of the next snapshot
   if (SNAP && w.dc->restore) {
-    // resume: recorded counters = new in-degree minus the arrivals recorded at
-    // the snapshot (the changed op's own counters start fresh; a counter of an op
-    // resized since the snapshot had no arrivals then), clocks, ready set
+    // resume: every counter some arrival had touched and that can still be
+    // read (a task still waiting on predecessors; every ring: its slot keeps
+    // the per-hop bytes once hop 0 is out) = new in-degree minus the arrivals at
+    // the snapshot.  The changed op's counters start fresh; an op resized since
+    // the snapshot had no arrivals then.  Tasks that ran or are in the ready set
+    // are never counted again.
     const char *src = w.dc->restore;
     const SnapLay sl = snap_layout(P);
     const SnapHdr *hd = (const SnapHdr *)src;
-    const int chg = w.dc->op, nl = hd->nlist;
-    const SnapEnt *ls = (const SnapEnt *)(src + sl.ls);
-    for (int e = lane; e < nl; e += 32) {
-      SnapEnt en = ls[e];
-      int o = en.code & 0xffff, kind = (en.code >> 16) & 3, k = en.code >> 18;
-      if (o == chg) continue;
-      const int *bs = kind == 2 ? w.gbase : w.fbase;
-      if (k >= bs[o + 1] - bs[o]) continue;
-      int c = (kind == 0 ? 0 : kind == 1 ? Tf : 2 * Tf) + bs[o] + k;
-      st.rem[c] -= (unsigned short)en.arr;
-      st.ready[c] = en.ready;
+    const int chg = w.dc->op, Tfo = hd->Tf, Go = hd->G;
+    const unsigned short *rmo = (const unsigned short *)(src + sl.rm);
+    const double *rdo = (const double *)(src + sl.rd);
+    const unsigned short *ido = w.dc->indeg0 + (size_t)hd->epoch * w.dc->ep_stride;
+    // the snapshot's layout, staged in the (still empty) ready-set area when it fits
+    const int *fbo = (const int *)(src + sl.fb), *gbo = (const int *)(src + sl.gb);
+    if ((size_t)(P.n_ops + 1) * 8 <= (size_t)w.rcap * sizeof(REnt)) {
+      int *sf = (int *)w.rs, *sg = sf + (P.n_ops + 1);
+      for (int j = lane; j <= P.n_ops; j += 32) { sf[j] = fbo[j]; if (FULL) sg[j] = gbo[j]; }
+      fbo = sf; gbo = sg;
+      __syncwarp();
     }
+    const int nco = FULL ? 2 * Tfo : Tfo;
+    for (int c8 = lane * 8; c8 < nco; c8 += 256) {  // 8 counters per lane per step
+      uint4 rv = *(const uint4 *)(rmo + c8), iv = *(const uint4 *)(ido + c8);
+      unsigned r2[4] = {rv.x, rv.y, rv.z, rv.w}, i2[4] = {iv.x, iv.y, iv.z, iv.w};
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int os = c8 + u;
+        unsigned re = (r2[u >> 1] >> ((u & 1) * 16)) & 0xffffu, ie = (i2[u >> 1] >> ((u & 1) * 16)) & 0xffffu;
+        if (os < nco && re > 0 && re < ie) {
+          int bw = os >= Tfo, x = bw ? os - Tfo : os;
+          int o = upper_bound(fbo, P.n_ops + 1, x) - 1;
+          int k = x - fbo[o];
+          if (o != chg && k < w.fbase[o + 1] - w.fbase[o]) {
+            int c = (bw ? Tf : 0) + w.fbase[o] + k;
+            st.rem[c] -= (unsigned short)(ie - re);
+            st.ready[c] = rdo[os];
+          }
+        }
+      }
+    }
+    if (FULL)
+      for (int og = lane; og < Go; og += 32) {
+        int o = upper_bound(gbo, P.n_ops + 1, og) - 1;
+        int si = og - gbo[o];
+        if (o != chg && si < w.gbase[o + 1] - w.gbase[o]) {
+          int c = 2 * Tf + w.gbase[o] + si, oc = 2 * Tfo + og;
+          st.rem[c] -= (unsigned short)(ido[oc] - rmo[oc]);
+          st.ready[c] = rdo[oc];
+        }
+      }
+    __syncwarp();
     const double *qco = (const double *)(src + sl.qc);
     for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = qco[q];
     n = hd->n;
@@ -1789,9 +1809,10 @@ struct DeltaBufs {
   ChainDelta *cd;          // [n]
   char *snaps;             // [n][nsnap][2] snapshot slots
   int *frb;                // [n][2 copies][forward, backward][n_ops] first rounds
-  unsigned short *indeg;   // [n][snap_counters]
+  unsigned short *indeg;   // [n][nsnap + 1 epochs][snap_counters_pad] in-degrees per simulation
   unsigned long long snap_bytes;
   int nsnap;
+  int exp;                 // experiments (PS_DELTA_EXP): 1 no snapshots, 2 snapshots but no resume
 };
 
 // Resume point of a proposal that changes op o:
@@ -1803,12 +1824,12 @@ struct DeltaBufs {
 __device__ inline int delta_prepare(const DevProb &P, const Tab &T, const W2 &w, const DeltaBufs &db, int chain,
                                     int o, double cost, bool full, bool from_scratch, int lane) {
   DeltaCtx *dc = w.dc;
-  const ChainDelta ch = dc->ch;
+  const ChainDelta &ch = dc->ch;  // (shared memory: read in place)
   int *fb0 = db.frb + (size_t)chain * 4 * P.n_ops;
   const int *fcur = fb0 + (size_t)(ch.fsel * 2) * P.n_ops, *bcur = fcur + P.n_ops;
   int *fnew = fb0 + (size_t)((ch.fsel ^ 1) * 2) * P.n_ops, *bnew = fnew + P.n_ops;
   int j = 0;
-  if (!from_scratch && ch.stride > 0 && ch.nvalid > 1 && P.min_exe > __dmul_rn(cost, 0x1p-50)) {
+  if (!from_scratch && db.exp != 2 && ch.stride > 0 && ch.nvalid > 1 && P.min_exe > __dmul_rn(cost, 0x1p-50)) {
     int i0 = T.op_in_off[o], i1 = T.op_in_off[o + 1];
     int R = i0 == i1 ? 0 : fcur[o];
     if (full) R = min(R, bcur[o]);
@@ -1821,12 +1842,20 @@ __device__ inline int delta_prepare(const DevProb &P, const Tab &T, const W2 &w,
     while (j > 0 && ((ch.bad >> j) & 1u)) --j;
   }
   __syncwarp();
+  // an epoch buffer no live snapshot of the current strategy refers to
+  unsigned used = 0;
+  for (int i = 1; i < ch.nvalid; ++i) used |= 1u << ch.ep[i];
+  const int epoch = __ffs(~used) - 1;  // nsnap + 1 buffers, at most nsnap - 1 in use
   if (lane == 0) {
-    dc->snap = ch.stride > 0 ? db.snaps + (size_t)chain * 2 * db.nsnap * db.snap_bytes : nullptr;
+    const unsigned long long eps = snap_counters_pad(P);
+    dc->indeg0 = db.indeg + (size_t)chain * (db.nsnap + 1) * eps;
+    dc->ep_stride = eps;
+    dc->epoch = epoch;
+    dc->snap = ch.stride > 0 && db.exp != 1 ? db.snaps + (size_t)chain * 2 * db.nsnap * db.snap_bytes : nullptr;
     dc->restore = j > 0 ? dc->snap + (2ull * j + ((ch.cur >> j) & 1u)) * db.snap_bytes : nullptr;
     dc->frnd = fnew; dc->brnd = bnew;
     dc->fsrc = fcur; dc->bsrc = bcur;
-    dc->indeg = db.indeg + (size_t)chain * snap_counters(P);
+    dc->indeg = db.indeg + ((size_t)chain * (db.nsnap + 1) + epoch) * eps;
     dc->snap_bytes = db.snap_bytes;
     dc->stride = ch.stride;
     dc->nsnap = db.nsnap;
@@ -1852,6 +1881,7 @@ __device__ inline void delta_commit(DeltaCtx *dc, int j, int lane) {
       ch.cur ^= mask;
       ch.bad = (ch.bad & ~mask) | (dc->bad & mask);
       ch.nvalid = last + 1;
+      for (int i = j + 1; i <= last; ++i) ch.ep[i] = (unsigned char)dc->epoch;
     }
     ch.fsel ^= 1;
   }
@@ -1865,7 +1895,6 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
        DeltaBufs db) {
   constexpr bool DELTA = (S & SIM_SNAP) != 0;
-  constexpr bool FULLM = (S & SIM_FULL) != 0;
   extern __shared__ __align__(16) char smem[];
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   int chain = blockIdx.x * wpb + wib;
@@ -2705,13 +2734,15 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     bool on = params->delta != 0 && P.min_exe > 0.0 && ns >= 4 && !getenv("PS_NO_DELTA");
     if (on) {
       m->db.nsnap = ns;
+      if (const char *e = getenv("PS_DELTA_EXP")) m->db.exp = atoi(e);
       m->db.snap_bytes = sb;
       CK(cudaMalloc(&m->db.cd, (size_t)n * sizeof(ChainDelta)));
       CK(cudaMemset(m->db.cd, 0, (size_t)n * sizeof(ChainDelta)));
       CK(cudaMalloc(&m->db.snaps, (size_t)n * 2 * ns * sb));
       CK(cudaMalloc(&m->db.frb, (size_t)n * 4 * P.n_ops * sizeof(int)));
       CK(cudaMemset(m->db.frb, 0x7f, (size_t)n * 4 * P.n_ops * sizeof(int)));  // "never ran"
-      CK(cudaMalloc(&m->db.indeg, (size_t)n * snap_counters(P) * sizeof(unsigned short)));
+      CK(cudaMalloc(&m->db.indeg, (size_t)n * (ns + 1) * snap_counters_pad(P) * sizeof(unsigned short)));
+      CK(cudaMemset(m->db.indeg, 0, (size_t)n * (ns + 1) * snap_counters_pad(P) * sizeof(unsigned short)));
     }
   }
   *out = m;
