@@ -424,7 +424,8 @@ struct ChainDelta {
 struct DeltaCtx {
   char *snap;              // this chain's snapshot slots: index i, copy b at snap + (2 i + b) snap_bytes
   const char *restore;     // snapshot to resume from (null: from time zero)
-  int *frnd, *brnd;        // this simulation's first round per op (forward / backward tasks)
+  int *frnd, *brnd;        // this simulation's first snapshot index per op at which one of its
+                           // forward / backward tasks had run (0x7fffffff: not seen)
   unsigned short *indeg;   // this simulation's dense counter in-degrees (global epoch buffer)
   const unsigned short *indeg0;  // epoch buffer 0 of the chain (snapshot headers name theirs)
   unsigned long long ep_stride;  // elements per epoch buffer
@@ -467,6 +468,7 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
   b += 256 + 128 + 16;                               // proposal staging, phase counters
   b += al16(sizeof(DeltaCtx));                       // delta context
+  b += al16(2 * (size_t)P.n_ops);                    // delta: ops seen running
   return b;
 }
 
@@ -493,6 +495,7 @@ struct W2 {
   unsigned char *oldasg;
   unsigned long long *ph;  // per-warp phase counters (PS_PHASES builds)
   DeltaCtx *dc;            // SIM_SNAP simulations: snapshots / resume
+  unsigned char *ran;      // SIM_SNAP: [2 n_ops] op seen to have run a forward / backward task
 };
 
 __device__ inline void carve_tab(char *base, const DevProb &P, Tab &t) {
@@ -574,6 +577,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.oldasg = (unsigned char *)take(256);
   w.ph = (unsigned long long *)take(128);
   w.dc = (DeltaCtx *)take(sizeof(DeltaCtx));
+  w.ran = (unsigned char *)take(2 * P.n_ops);
   w.rcap = P.cap;
   w.opmin = nullptr;
   w.tr = nullptr;
@@ -642,15 +646,20 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 
 // First rounds of a delta simulation: the resumed strategy's below the resume
 // round (those ops ran identically), unset above it.
-__device__ inline void delta_first_rounds(const DevProb &P, DeltaCtx *dc, int lane) {
+__device__ inline void delta_first_rounds(const DevProb &P, const W2 &w, int lane) {
+  DeltaCtx *dc = w.dc;
   __syncwarp();
-  const int r0 = dc->r0;
+  const int j = dc->restore_idx;
   const int *fs = dc->fsrc, *bs = dc->bsrc;
   int *fd = dc->frnd, *bd = dc->brnd;
   for (int i = lane; i < P.n_ops; i += 32) {
-    int a = fs && r0 > 0 ? fs[i] : 0x7fffffff, b = bs && r0 > 0 ? bs[i] : 0x7fffffff;
-    fd[i] = a < r0 ? a : 0x7fffffff;
-    bd[i] = b < r0 ? b : 0x7fffffff;
+    int a = fs && j > 0 ? fs[i] : 0x7fffffff, b = bs && j > 0 ? bs[i] : 0x7fffffff;
+    a = a <= j ? a : 0x7fffffff;
+    b = b <= j ? b : 0x7fffffff;
+    fd[i] = a;
+    bd[i] = b;
+    w.ran[i] = a <= j;
+    w.ran[P.n_ops + i] = b <= j;
   }
   __syncwarp();
 }
@@ -665,7 +674,7 @@ __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &
   W2 wg = w;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    if (M & SIM_SNAP) delta_first_rounds(P, w.dc, lane);
+    if (M & SIM_SNAP) delta_first_rounds(P, w, lane);
     o = warp_simulate2<M>(P, T, wg, L, gscratch, lane);
     if (o.status != PS_STATUS_CAPACITY) break;
     wg = with_global_ready_set(P, gscratch, w);
@@ -937,11 +946,40 @@ __device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const 
     if (!ok) dc->bad |= 1u << i;
   }
   if (!ok) return;
+  // ops seen to have run a task before this round: a task that ran has no
+  // remaining count and is not in the ready set (ready-set op tasks are marked
+  // with a count of 0xffff meanwhile; the raw copy below is taken before)
+  copy16(dst + sl.rm, st.rem, 2 * (size_t)nc, lane);
+  __syncwarp();
+  for (int j = lane; j < n; j += 32) {
+    unsigned kd = key_kind(w.rs[j].k);
+    if (kd == KIND_OP || kd == KIND_OP_BWD)
+      st.rem[(kd == KIND_OP ? 0 : st.Tf) + w.fbase[key_a(w.rs[j].k)] + key_c(w.rs[j].k)] = 0xffff;
+  }
+  __syncwarp();
+  const int nb = full ? 2 : 1;
+  for (int x = lane; x < nb * P.n_ops; x += 32) {
+    if (w.ran[x]) continue;
+    int o = x < P.n_ops ? x : x - P.n_ops;
+    int base = (x < P.n_ops ? 0 : st.Tf) + w.fbase[o], sz = w.fbase[o + 1] - w.fbase[o];
+    bool r = false;
+    for (int k = 0; k < sz && !r; ++k) r = st.rem[base + k] == 0;
+    if (r) {
+      w.ran[x] = 1;
+      (x < P.n_ops ? dc->frnd : dc->brnd)[o] = i;
+    }
+  }
+  __syncwarp();
+  for (int j = lane; j < n; j += 32) {
+    unsigned kd = key_kind(w.rs[j].k);
+    if (kd == KIND_OP || kd == KIND_OP_BWD)
+      st.rem[(kd == KIND_OP ? 0 : st.Tf) + w.fbase[key_a(w.rs[j].k)] + key_c(w.rs[j].k)] = 0;
+  }
+  __syncwarp();
   copy16(dst + sl.fb, w.fbase, 4 * (size_t)(P.n_ops + 1), lane);
   if (full) copy16(dst + sl.gb, w.gbase, 4 * (size_t)(P.n_ops + 1), lane);
   copy16(dst + sl.qc, w.qclock, 8 * (size_t)P.n_queues, lane);
   copy16(dst + sl.rs, w.rs, 32 * (size_t)n, lane);
-  copy16(dst + sl.rm, st.rem, 2 * (size_t)nc, lane);
   copy16(dst + sl.rd, st.ready, 8 * (size_t)nc, lane);
 }
 
@@ -1001,7 +1039,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     }
     st.rem[s] = (unsigned short)indeg;
     st.ready[s] = 0.0;
+#ifndef PS_DELTA_NOINDEG
     if (SNAP) w.dc->indeg[s] = (unsigned short)indeg;
+#endif
     if (FULL) {
       int outd = 1;
       for (int i = T.op_out_off[o]; i < T.op_out_off[o + 1]; ++i) {
@@ -1010,7 +1050,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       st.rem[Tf + s] = (unsigned short)outd;
       st.ready[Tf + s] = 0.0;
+#ifndef PS_DELTA_NOINDEG
       if (SNAP) w.dc->indeg[Tf + s] = (unsigned short)outd;
+#endif
       int pm = T.op_param_mask[o];
       if (pm >= 0) {
         int g = w.gmap[o];
@@ -1087,7 +1129,15 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = qco[q];
     n = hd->n;
     const REnt *rso = (const REnt *)(src + sl.rs);
-    for (int i = lane; i < n; i += 32) w.rs[i] = rso[i];
+    for (int i = lane; i < n; i += 32) {
+      REnt r = rso[i];
+      w.rs[i] = r;
+      // a ready op task has no remaining count (the snapshots' "has run" test
+      // reads it: ran = no remaining count and not in the ready set)
+      unsigned kd = key_kind(r.k);
+      if (kd == KIND_OP || (FULL && kd == KIND_OP_BWD))
+        st.rem[(kd == KIND_OP ? 0 : Tf) + w.fbase[key_a(r.k)] + key_c(r.k)] = 0;
+    }
     if (lane == 0) out.makespan = hd->makespan;
     round = hd->round;
     __syncwarp();
@@ -1340,11 +1390,6 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         end = start + myexe;
         w.qclock[myq] = end;
       }
-    }
-    if (SNAP && mine) {
-      unsigned kd = key_kind(mykey);
-      if (kd == KIND_OP) atomicMin(&w.dc->frnd[key_a(mykey)], round);
-      else if (kd == KIND_OP_BWD) atomicMin(&w.dc->brnd[key_a(mykey)], round);
     }
     if (mine) {
       if (end > out.makespan) out.makespan = end;
@@ -1813,6 +1858,8 @@ struct DeltaBufs {
   unsigned long long snap_bytes;
   int nsnap;
   int exp;                 // experiments (PS_DELTA_EXP): 1 no snapshots, 2 snapshots but no resume
+  int *dbg;                // PS_DELTA_TRACE: [n][dbg_cap][8] per proposal (o, j, R, rounds, nvalid, stride, ...)
+  int dbg_cap;
 };
 
 // Resume point of a proposal that changes op o:
@@ -1830,6 +1877,7 @@ __device__ inline int delta_prepare(const DevProb &P, const Tab &T, const W2 &w,
   int *fnew = fb0 + (size_t)((ch.fsel ^ 1) * 2) * P.n_ops, *bnew = fnew + P.n_ops;
   int j = 0;
   if (!from_scratch && db.exp != 2 && ch.stride > 0 && ch.nvalid > 1 && P.min_exe > __dmul_rn(cost, 0x1p-50)) {
+    // (first snapshot index at which a task with an o-dependent successor list had run) - 1
     int i0 = T.op_in_off[o], i1 = T.op_in_off[o + 1];
     int R = i0 == i1 ? 0 : fcur[o];
     if (full) R = min(R, bcur[o]);
@@ -1838,7 +1886,7 @@ __device__ inline int delta_prepare(const DevProb &P, const Tab &T, const W2 &w,
       for (int i = T.op_out_off[o] + lane; i < T.op_out_off[o + 1]; i += 32)
         R = min(R, bcur[T.pair_dst[T.op_out_pairs[i]]]);
     R = __reduce_min_sync(FULLMASK, R);
-    j = max(0, min(R / ch.stride, ch.nvalid - 1));
+    j = max(0, min(R - 1, ch.nvalid - 1));
     while (j > 0 && ((ch.bad >> j) & 1u)) --j;
   }
   __syncwarp();
@@ -1992,6 +2040,11 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
         }
         so = simulate_any<S>(P, T, w, lay, gs, lane);
         if (so.status != PS_STATUS_OK) break;
+        if (DELTA && db.dbg && lane == 0 && it >= 0 && cs.proposals < db.dbg_cap) {
+          int *d = db.dbg + ((size_t)chain * db.dbg_cap + cs.proposals) * 8;
+          d[0] = o; d[1] = dj; d[2] = w.dc->ch.nvalid; d[3] = w.dc->rounds; d[4] = w.dc->ch.stride;
+          d[5] = w.dc->last; d[6] = (int)w.dc->ch.bad; d[7] = w.dc->ch.fsel;
+        }
         if (DELTA) {
           if (lane == 0) {
             ChainDelta &ch = w.dc->ch;
@@ -2735,6 +2788,11 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     if (on) {
       m->db.nsnap = ns;
       if (const char *e = getenv("PS_DELTA_EXP")) m->db.exp = atoi(e);
+      if (const char *e = getenv("PS_DELTA_TRACE")) {
+        m->db.dbg_cap = atoi(e);
+        CK(cudaMalloc(&m->db.dbg, (size_t)n * m->db.dbg_cap * 8 * sizeof(int)));
+        CK(cudaMemset(m->db.dbg, 0xff, (size_t)n * m->db.dbg_cap * 8 * sizeof(int)));
+      }
       m->db.snap_bytes = sb;
       CK(cudaMalloc(&m->db.cd, (size_t)n * sizeof(ChainDelta)));
       CK(cudaMemset(m->db.cd, 0, (size_t)n * sizeof(ChainDelta)));
@@ -2832,6 +2890,16 @@ int ps_debug_delta_state(ps_mcmc *m, void *out) {
   return PS_OK;
 }
 
+// debug (PS_DELTA_TRACE=cap): per chain and proposal (op, resume index, nvalid, rounds, stride, last, bad, fsel),
+// then the chain's first-index buffers [2][2][n_ops]
+int ps_debug_delta_trace(ps_mcmc *m, int32_t *out, int32_t *frb) {
+  if (!m || !m->db.dbg) return fail(PS_ERR_INVALID, "PS_DELTA_TRACE was not set");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, m->db.dbg, (size_t)m->n * m->db.dbg_cap * 8 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (frb) CK(cudaMemcpy(frb, m->db.frb, (size_t)m->n * 4 * m->prob->P.n_ops * sizeof(int), cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
 int ps_debug_tcyc(long long *out) {
 #ifdef PS_TCYC
   CK(cudaDeviceSynchronize());
@@ -2894,7 +2962,7 @@ void ps_mcmc_destroy(ps_mcmc *m) {
     cudaFree(m->d_best); cudaFree(m->d_bestc);
   }
   cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok);
-  cudaFree(m->db.cd); cudaFree(m->db.snaps); cudaFree(m->db.frb); cudaFree(m->db.indeg);
+  cudaFree(m->db.dbg); cudaFree(m->db.cd); cudaFree(m->db.snaps); cudaFree(m->db.frb); cudaFree(m->db.indeg);
   if (m->scratch) {  // keep the largest chain scratch for the problem's next handle
     if (m->scratch_bytes >= m->prob->mcmc_scratch_bytes) {
       cudaFree(m->prob->mcmc_scratch);
