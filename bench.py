@@ -9,9 +9,18 @@ A step = every chain makes ``--proposals`` Metropolis proposals, each scored
 by a full GPU re-simulation of the changed strategy (one k_mcmc launch);
 value = proposals (= strategy evaluations) of all ranks / max-over-ranks time.
 
+Proposals are scored by checkpointed delta evaluation (the B200 form of the
+reference's update_task_graph + delta_simulate); ``full_eval`` reports full
+evaluations (build + full simulate, ``k_simulate_batch``) of the chains'
+strategies beside it, and ``configs`` the other BASELINE configs (AlexNet,
+ResNet-101 on 64 devices, NMT-40 on 64 devices, random DAGs of 1k / 10k ops)
+with their own rooflines.
+
 ``--impl reference`` times the CPU restatement of the reference path
 (oracle/parasim_oracle.c: rebuild + full simulate per proposal) on all host
-threads, on a bounded sample of the same chains, rank 0 only.
+threads, on a wall-clock-bounded sample of the same chains, rank 0 only; the
+unmodified Python reference (baseline/_ref, ``mcmc_search(polish=False)`` over
+a process pool) is timed beside it as ``python_reference`` when installed.
 """
 
 from __future__ import annotations
@@ -24,7 +33,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -53,6 +61,10 @@ def parse():
                     help="score every proposal from time zero instead of resuming from a snapshot")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--py-ref-seconds", type=float, default=8.0,
+                    help="wall time of the Python-reference leg (0: skip)")
+    ap.add_argument("--extra", default="alexnet,resnet,nmt,random1k,random10k",
+                    help="other BASELINE configs measured after the headline ('none': skip)")
     return ap.parse_args()
 
 
@@ -67,6 +79,8 @@ def workload(name, ops=1000):
     if name == "nmt":
         return (ps.nmt_like(steps=40, layers=2, batch=64, hidden=1024, vocab=32768), ps.multi_node_topology(16, 4), 8,
                 "NMT-40 on 16x4 GPUs")
+    if name.startswith("random") and name[6:].rstrip("k").isdigit():
+        ops = int(name[6:].rstrip("k")) * (1000 if name.endswith("k") else 1)
     return ps.random_dag(ops, seed=1000), ps.multi_node_topology(4, 4), 4, f"random DAG {ops} ops on 4x4 GPUs"
 
 
@@ -143,21 +157,55 @@ def cpu_baseline(g, topo, prof, mode, md, init, seeds, seconds, threads):
     from oracle.oracle_io import Oracle
     orc = Oracle()
     n = min(len(init), threads)
-    times = []
-    for p in (1, 3):  # two calibration points: the slope is the per-proposal cost
-        t0 = time.perf_counter()
-        orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], p, md, rng_mode="philox", threads=threads)
-        times.append(time.perf_counter() - t0)
-    per_prop = max(1e-6, (times[1] - times[0]) / 2)
-    props = max(2, int(seconds / per_prop))
+    # wall-clock bounded: every chain stops between proposals at the deadline
     t0 = time.perf_counter()
-    out = orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], props, md, rng_mode="philox", threads=threads)
+    out = orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], 200000, md, rng_mode="philox", threads=threads,
+                   deadline_s=seconds)
     dt = time.perf_counter() - t0
     total = float(out["summary"][:, 2].sum())
     # the initial full evaluation of each chain is counted as an evaluation too
     evals = total + n
     return {"value": evals / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n} chains x {props} proposals ({mode}, rebuild+full simulate per proposal), {dt:.1f}s"}
+            "sample": (f"{n} chains x {total / n:.0f} proposals on average ({mode}, rebuild+full simulate per "
+                       f"proposal, wall-clock bounded), {dt:.1f}s")}
+
+
+def _py_ref_chain(job):
+    """One chain of the unmodified reference (baseline/_ref): mcmc_search with
+    a single initial strategy, seed 1000003*c (its chain-c seed), polish off."""
+    ref_path, g_json, topo_json, s_json, seed, mode, md, seconds = job
+    sys.path.insert(0, ref_path)
+    import parasim
+    from parasim import formats as rf
+    g, topo = rf.graph_from_json(g_json), rf.topology_from_json(topo_json)
+    params = parasim.SearchParams(budget_seconds=seconds, seed=seed, max_degree=md, mode=mode, polish=False,
+                                  initial=[rf.strategy_from_json(s_json)], stagnation_floor=1e9)
+    t0 = time.perf_counter()
+    rep = parasim.mcmc_search(g, topo, parasim.CostProfile(), params)
+    return rep.proposals + 1, time.perf_counter() - t0
+
+
+def python_reference(g, topo, mode, md, init, seconds, procs):
+    """The reference's own Python path: mcmc_search(polish=False),
+    one chain per process over all host cores, wall-clock bounded by its own
+    budget rule; evaluations = proposals + the initial full simulation."""
+    ref_path = os.path.join(ROOT, "baseline", "_ref")
+    if seconds <= 0 or not os.path.isdir(os.path.join(ref_path, "parasim")):
+        return None
+    import multiprocessing as mproc
+    from paper_1807_05358_b200 import formats
+    gj, tj = formats.graph_to_json(g), formats.topology_to_json(topo)
+    n = min(len(init), procs)
+    jobs = [(ref_path, gj, tj, formats.strategy_to_json(init[c]), 1000003 * c, mode, md, seconds) for c in range(n)]
+    t0 = time.perf_counter()
+    with mproc.get_context("spawn").Pool(n) as pool:
+        res = pool.map(_py_ref_chain, jobs)
+    wall = time.perf_counter() - t0
+    evals = sum(e for e, _ in res)
+    busy = max(t for _, t in res)
+    return {"value": evals / busy, "unit": UNIT, "cores": n, "kind": "reference (unmodified Python, baseline/_ref)",
+            "sample": (f"{n} chains, mcmc_search(polish=False, budget_seconds={seconds:g}) one per process, "
+                       f"{evals} evaluations in {busy:.1f}s of search ({wall:.1f}s with process start-up)")}
 
 
 def run_reference(args):
@@ -172,10 +220,15 @@ def run_reference(args):
     seeds = [1000003 * c for c in range(threads)]
     vals = []
     for i in range(args.warmup + args.steps):
-        res = cpu_baseline(g, topo, prof, args.mode, md, init, seeds, max(2.0, args.cpu_seconds / 3), threads)
+        # warm-up steps are short (1 s); timed steps are wall-clock-bounded samples
+        secs = 1.0 if i < args.warmup else max(2.0, args.cpu_seconds / 4)
+        res = cpu_baseline(g, topo, prof, args.mode, md, init, seeds, secs, threads)
         if i >= args.warmup:
             vals.append(res["value"])
     v = statistics.mean(vals)
+    py = python_reference(g, topo, args.mode, md, init, args.py_ref_seconds, threads)
+    if py is not None:
+        res = {**res, "python_reference": py}
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
@@ -185,13 +238,146 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+class Chains:
+    """One MCMC handle over C chains of a workload, set up through the C ABI."""
+
+    def __init__(self, name, mode, C, first, delta, device, ops=1000, distinct=None):
+        import paper_1807_05358_b200 as ps
+        from paper_1807_05358_b200 import _native as nat
+        from paper_1807_05358_b200.lowering import lower
+        from paper_1807_05358_b200.search import fit_capacity
+        self.ps, self.nat, self.L = ps, nat, nat.lib()
+        g, topo, md, desc = workload(name, ops)
+        self.g, self.topo, self.md, self.desc, self.mode, self.C = g, topo, md, desc, mode, C
+        self.prof = ps.CostProfile()
+        if distinct is None:
+            init = initial_strategies(g, topo, md, first, C)
+            starts = init
+        else:
+            # very large graphs: `distinct` starts (DP + random) tiled over the
+            # chains; every chain still has its own Philox stream
+            starts = initial_strategies(g, topo, md, 0, distinct)
+            init = [starts[i % distinct] for i in range(C)]
+        self.init = init
+        # every rank lowers the same map set (the data-parallel start's maps first), so
+        # encoded strategies mean the same thing on every GPU for the final exchange
+        low = lower(g, topo, self.prof, mode, max_degree=md,
+                    strategies=[ps.data_parallel_strategy(g, topo)] + list(starts), device=device)
+        maps = np.zeros((C, low.n_ops), dtype=np.int32)
+        asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+        enc = {}
+        for i, s in enumerate(init):
+            if id(s) not in enc:
+                enc[id(s)] = low.encode(s)
+            maps[i], asg[i] = enc[id(s)]
+        n_fit = C if distinct is None else distinct
+        low = fit_capacity(low, maps[:n_fit], asg[:n_fit])  # ready-set capacity from a pilot evaluation
+        self.low, self.maps, self.asg = low, maps, asg
+        self.seeds = np.array([1000003 * (first + i) for i in range(C)], dtype=np.uint64)
+        self.mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0, 1 if delta else 0)
+        self.h = self.create(maps, asg, self.seeds)
+
+    def create(self, maps, asg, seeds):
+        nat = self.nat
+        h = ctypes.c_void_p()
+        nat.check(self.L.ps_mcmc_create(self.low.handle(), ctypes.byref(self.mp), self.C, nat.ptr(maps), nat.ptr(asg),
+                                        nat.ptr(seeds), None, ctypes.byref(h)), "ps_mcmc_create")
+        return h
+
+    def step(self, h, stream_handle, budget_ns, proposals):
+        nat = self.nat
+        if budget_ns:
+            nat.check(self.L.ps_mcmc_run_budget(h, 1 << 30, budget_ns, stream_handle), "ps_mcmc_run_budget")
+        else:
+            nat.check(self.L.ps_mcmc_run(h, proposals, stream_handle), "ps_mcmc_run")
+
+    def summary(self, h=None):
+        s = (self.nat.PsChainSummary * self.C)()
+        self.nat.check(self.L.ps_mcmc_read(h or self.h, s, None, None, None, None), "ps_mcmc_read")
+        return s
+
+    def state(self):
+        sm = np.zeros((self.C, self.low.n_ops), dtype=np.int32)
+        sa = np.zeros((self.C, self.low.n_slots), dtype=np.uint8)
+        self.nat.check(self.L.ps_mcmc_read_state(self.h, self.nat.ptr(sm), self.nat.ptr(sa)), "ps_mcmc_read_state")
+        return sm, sa
+
+    def bytes_per_eval(self, sm, sa, samples):
+        """Algorithmic bytes per evaluation: 32 B per task + 4 B per dependency
+        (SURVEY 8d), averaged over a sample of the chains' live strategies
+        (traced on the GPU)."""
+        from paper_1807_05358_b200.taskgraph import _bind
+        te = []
+        for i in range(0, self.C, max(1, self.C // samples)):
+            tg = self.ps.TaskGraph(self.g, self.topo, self.low.decode(sm[i], sa[i]), self.prof, self.mode)
+            _bind(tg, self.low)
+            T = len(tg.tasks)
+            E = sum(len(t.outputs) for t in tg.tasks.values())
+            te.append((T, E))
+        T_avg = statistics.mean(t for t, _ in te)
+        E_avg = statistics.mean(e for _, e in te)
+        return 32.0 * T_avg + 4.0 * E_avg, T_avg, E_avg
+
+    def destroy(self):
+        self.L.ps_mcmc_destroy(self.h)
+
+
+def timed_steps(ch, h, stream, sh, steps, budget_ns, proposals, flush):
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a_, b_ in ev:
+        a_.record(stream)
+        ch.step(h, sh, budget_ns, proposals)
+        b_.record(stream)
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+    torch.cuda.synchronize()
+    return [a_.elapsed_time(b_) for a_, b_ in ev]
+
+
+EXTRA = {  # name: (chains, step budget ms, distinct starts or None, trace samples)
+    "alexnet": (1024, 100.0, None, 16),
+    "resnet": (1024, 100.0, None, 8),
+    "nmt": (4096, 300.0, 64, 4),
+    "random1k": (4096, 300.0, 64, 4),
+    "random10k": (4096, 1000.0, 16, 2),
+}
+
+
+def measure_extra(name, mode, device, stream, sh, flush, peak, steps=3, warmup=2):
+    C, bms, distinct, samples = EXTRA[name]
+    ch = Chains(name, mode, C, 0, True, device, distinct=distinct)
+    budget_ns = int(bms * 1e6)
+    for _ in range(warmup):
+        ch.step(ch.h, sh, budget_ns, 0)
+    import torch
+    torch.cuda.synchronize()
+    s0 = ch.summary()
+    ms = timed_steps(ch, ch.h, stream, sh, steps, budget_ns, 0, flush)
+    s1 = ch.summary()
+    evals = sum(s.proposals for s in s1) - sum(s.proposals for s in s0)
+    run = sum(s.rounds_run for s in s1) - sum(s.rounds_run for s in s0)
+    reused = sum(s.rounds_reused for s in s1) - sum(s.rounds_reused for s in s0)
+    sm, sa = ch.state()
+    bpe, T, E = ch.bytes_per_eval(sm, sa, samples)
+    info = ch.low.info()
+    ch.destroy()
+    v = evals / (sum(ms) / 1e3)
+    achieved = bpe * v / 1e9
+    return {"workload": ch.desc, "mode": mode, "max_degree": ch.md, "chains": C, "value": v, "unit": UNIT,
+            "tasks_per_s": v * T, "ms_per_step": sum(ms) / steps, "steps": steps,
+            "step": f"time-boxed {bms:g} ms", "tasks_per_eval": round(T, 1), "deps_per_eval": round(E, 1),
+            "delta_reused_fraction": reused / max(1, run + reused),
+            "failures": sum(1 for s in s1 if s.status != ch.nat.PS_STATUS_OK),
+            "resident_warps_per_sm": info.resident_warps_per_sm, "ready_capacity": info.ready_capacity,
+            "starts": "data-parallel + random" + (f" ({distinct} distinct, tiled)" if distinct else ""),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "note": f"B_eval = 32*T + 4*E = {bpe:.0f} B"}}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    import paper_1807_05358_b200 as ps
     from paper_1807_05358_b200 import _native as nat
-    from paper_1807_05358_b200.lowering import lower
-    from paper_1807_05358_b200.rng import mt_state_words  # noqa: F401
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -207,82 +393,34 @@ def run_ours(args):
             dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    g, topo, md, desc = workload(args.config, args.ops)
-    prof = ps.CostProfile()
     C = args.chains
     first = rank * C
-    init = initial_strategies(g, topo, md, first, C)
-    from paper_1807_05358_b200.search import fit_capacity
-    # every rank lowers the same map set (the data-parallel start's maps first), so
-    # encoded strategies mean the same thing on every GPU for the final exchange
-    low = lower(g, topo, prof, args.mode, max_degree=md, strategies=[ps.data_parallel_strategy(g, topo)] + init,
-                device=local)
-    L = nat.lib()
-    maps = np.zeros((C, low.n_ops), dtype=np.int32)
-    asg = np.zeros((C, low.n_slots), dtype=np.uint8)
-    for i, s in enumerate(init):
-        low.encode(s, maps[i], asg[i])
-    low = fit_capacity(low, maps, asg)  # ready-set capacity from a pilot evaluation of the starts
+    ch = Chains(args.config, args.mode, C, first, not args.no_delta, local, ops=args.ops)
+    L, low, g, topo, md, desc, prof = ch.L, ch.low, ch.g, ch.topo, ch.md, ch.desc, ch.prof
     info = low.info()
-    seeds = np.array([1000003 * (first + i) for i in range(C)], dtype=np.uint64)
-    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0, 0 if args.no_delta else 1)
-    h = ctypes.c_void_p()
-    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(seeds), None,
-                               ctypes.byref(h)), "ps_mcmc_create")
     stream = torch.cuda.current_stream(dev)
     sh = ctypes.c_void_p(stream.cuda_stream)
     P = args.proposals
     budget_ns = int(args.budget_ms * 1e6)
-
-    def run_step(handle):
-        if budget_ns:
-            nat.check(L.ps_mcmc_run_budget(handle, 1 << 30, budget_ns, sh), "ps_mcmc_run_budget")
-        else:
-            nat.check(L.ps_mcmc_run(handle, P, sh), "ps_mcmc_run")
-
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     # first launch also scores the initial strategies (warm-up)
     for _ in range(args.warmup):
-        run_step(h)
+        ch.step(ch.h, sh, budget_ns, P)
         flush.zero_()
     torch.cuda.synchronize(dev)
-    # algorithmic bytes per evaluation: 32 B per task + 4 B per dependency, averaged
-    # over a sample of the chains' live strategies (traced on the GPU)
-    sm = np.zeros((C, low.n_ops), dtype=np.int32)
-    sa = np.zeros((C, low.n_slots), dtype=np.uint8)
-    nat.check(L.ps_mcmc_read_state(h, nat.ptr(sm), nat.ptr(sa)), "ps_mcmc_read_state")
-    tasks_edges = []
-    for i in range(0, C, max(1, C // 16)):
-        tg = ps.TaskGraph(g, topo, low.decode(sm[i], sa[i]), prof, args.mode)
-        from paper_1807_05358_b200.taskgraph import _bind
-        _bind(tg, low)
-        T = len(tg.tasks)
-        E = sum(len(t.outputs) for t in tg.tasks.values())
-        tasks_edges.append((T, E))
-    T_avg = statistics.mean(t for t, _ in tasks_edges)
-    E_avg = statistics.mean(e for _, e in tasks_edges)
-    bytes_per_eval = 32.0 * T_avg + 4.0 * E_avg
-    summ0 = (nat.PsChainSummary * C)()
-    nat.check(L.ps_mcmc_read(h, summ0, None, None, None, None), "ps_mcmc_read")
+    sm, sa = ch.state()
+    bytes_per_eval, T_avg, E_avg = ch.bytes_per_eval(sm, sa, 16)
+    summ0 = ch.summary()
     props0 = sum(s.proposals for s in summ0)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            starts[i].record(stream)
-            run_step(h)
-            ends[i].record(stream)
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-        torch.cuda.synchronize(dev)
+        step_ms = timed_steps(ch, ch.h, stream, sh, args.steps, budget_ns, P, flush)
     if world > 1:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
-    summ = (nat.PsChainSummary * C)()
-    nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+    summ = ch.summary()
     evals = sum(s.proposals for s in summ) - props0
     rounds_run = sum(s.rounds_run for s in summ) - sum(s.rounds_run for s in summ0)
     rounds_reused = sum(s.rounds_reused for s in summ) - sum(s.rounds_reused for s in summ0)
@@ -290,10 +428,10 @@ def run_ours(args):
     # best strategy across chains: device argmin, then the one cross-GPU exchange
     from paper_1807_05358_b200.parallel import global_best
     bc, bi = ctypes.c_double(), ctypes.c_int32()
-    nat.check(L.ps_mcmc_best(h, ctypes.byref(bc), ctypes.byref(bi)), "ps_mcmc_best")
+    nat.check(L.ps_mcmc_best(ch.h, ctypes.byref(bc), ctypes.byref(bi)), "ps_mcmc_best")
     bm_all = np.zeros((C, low.n_ops), dtype=np.int32)
     ba_all = np.zeros((C, low.n_slots), dtype=np.uint8)
-    nat.check(L.ps_mcmc_read(h, None, nat.ptr(bm_all), nat.ptr(ba_all), None, None), "ps_mcmc_read")
+    nat.check(L.ps_mcmc_read(ch.h, None, nat.ptr(bm_all), nat.ptr(ba_all), None, None), "ps_mcmc_read")
     li = int(bi.value)
     win_cost, win_chain, win_map, win_asg = global_best(
         float(bc.value), first + li if li >= 0 else -1, bm_all[max(li, 0)], ba_all[max(li, 0)], device=dev)
@@ -307,8 +445,13 @@ def run_ours(args):
     all_evals = float(ev.item())
     value = all_evals / (total_ms / 1e3)
 
-    # ---- e2e: the C-ABI with host buffers, H2D of the step's inputs and D2H of its results inside the timing
+    # ---- e2e: the C-ABI with host buffers, H2D of the step's inputs and D2H of
+    # its results inside the timing.  Each step resumes the chains' warm live
+    # strategies (read back after the timed region) on a fresh handle -- create
+    # (H2D), one time-boxed segment, read summaries + best strategies (D2H) --
+    # so it runs the same search phase as `value`, plus the handle set-up.
     e2e_times = []
+    wm, wa = ch.state()
 
     def pinned(a):  # page-locked host copy (numpy view of pinned memory)
         t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
@@ -316,7 +459,7 @@ def run_ours(args):
         out[...] = a
         return out, t
 
-    (pmaps, _t1), (pasg, _t2), (pseeds, _t3) = pinned(maps), pinned(asg), pinned(seeds)
+    (pmaps, _t1), (pasg, _t2), (pseeds, _t3) = pinned(wm), pinned(wa), pinned(ch.seeds + np.uint64(7))
     h2d = pmaps.nbytes + pasg.nbytes + pseeds.nbytes
     best_maps, _t4 = pinned(np.zeros((C, low.n_ops), dtype=np.int32))
     best_asg, _t5 = pinned(np.zeros((C, low.n_slots), dtype=np.uint8))
@@ -327,11 +470,9 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        h2 = ctypes.c_void_p()
-        nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(pmaps), nat.ptr(pasg), nat.ptr(pseeds),
-                                   None, ctypes.byref(h2)), "ps_mcmc_create")
+        h2 = ch.create(pmaps, pasg, pseeds)
         t1 = time.perf_counter()
-        run_step(h2)
+        ch.step(h2, sh, budget_ns, P)
         t2 = time.perf_counter()
         s2 = (nat.PsChainSummary * C)()
         nat.check(L.ps_mcmc_read(h2, s2, nat.ptr(best_maps), nat.ptr(best_asg), None, None), "ps_mcmc_read")
@@ -342,8 +483,6 @@ def run_ours(args):
         L.ps_mcmc_destroy(h2)
         if i >= args.warmup:
             e2e_times.append(dt)
-            if os.environ.get("PS_BENCH_VERBOSE"):
-                print(f"e2e step {i}: {dt * 1e3:.2f} ms", file=sys.stderr)
             # evaluations = the initial scoring of every chain + its proposals
             e2e_evals += sum(s.proposals for s in s2) + C
     e2e_t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
@@ -394,6 +533,7 @@ def run_ours(args):
         "config": {"workload": desc, "mode": args.mode, "max_degree": md, "chains_per_gpu": C,
                    "step": (f"time-boxed: every chain proposes for {args.budget_ms:g} ms of device time"
                             if budget_ns else f"{P} proposals per chain"),
+                   "evaluation": "delta (resume from a snapshot)" if not args.no_delta else "full re-simulation",
                    "proposals_per_step": round(evals / args.steps, 1),
                    "rng": "philox", "l2": "flushed between steps (256 MB write)",
                    "tasks_per_eval": round(T_avg, 1), "deps_per_eval": round(E_avg, 1),
@@ -405,21 +545,38 @@ def run_ours(args):
                      "note": (f"B_eval = 32*T + 4*E = {bytes_per_eval:.0f} B per evaluation (SURVEY 8d), "
                               f"{evals / args.steps:.0f} evaluations per launch; peak {peak_src}; "
                               "traffic from profiles/traffic.json (ncu)")},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "note": "per step: ps_mcmc_create from the warm chains' strategies (pinned host buffers), one "
+                        "time-boxed segment, ps_mcmc_read of summaries + best strategies; the initial scoring "
+                        "of each chain counts as an evaluation"},
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
         "delta": {"enabled": not args.no_delta, "rounds_run": int(rounds_run), "rounds_reused": int(rounds_reused),
                   "reused_fraction": rounds_reused / max(1, rounds_run + rounds_reused)},
+        "evals_by_kind": {"delta_per_s": value if not args.no_delta else None, "full_per_s": full_value,
+                          "note": "delta = MCMC proposals resumed from a snapshot (value); full = build + full "
+                                  "simulation of given strategies (full_eval)"},
         "chain_failures": bad, "best_makespan": float(best.item()), "best_chain": win_chain,
         "full_eval": {"value": full_value, "unit": UNIT, "candidates_per_launch": FB, "failures": bad_full,
                       "note": "full evaluations (no search) of the chains' current strategies (8 adjacent copies each), "
                               "one k_simulate_batch launch per step, device-resident inputs"},
     }
-    L.ps_mcmc_destroy(h)
+    ch.destroy()
+    extras = [x for x in args.extra.split(",") if x and x != "none"] if world == 1 else []
+    if extras:
+        line["configs"] = {}
+        for name in extras:
+            try:
+                line["configs"][name] = measure_extra(name, args.mode, local, stream, sh, flush, peak)
+            except Exception as exc:  # noqa: BLE001 - report, keep the headline
+                line["configs"][name] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        line["cpu_baseline"] = cpu_baseline(g, topo, prof, args.mode, md, init, [1000003 * c for c in range(C)],
+        line["cpu_baseline"] = cpu_baseline(g, topo, prof, args.mode, md, ch.init, [1000003 * c for c in range(C)],
                                             args.cpu_seconds, threads)
+        py = python_reference(g, topo, args.mode, md, ch.init, args.py_ref_seconds, threads)
+        if py is not None:
+            line["cpu_baseline"]["python_reference"] = py
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

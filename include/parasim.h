@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 2
+#define PS_ABI_VERSION 3
 #define PS_MAXDIM 5
 
 enum {
@@ -196,6 +196,24 @@ int ps_mcmc_run(ps_mcmc *m, int proposals, void *stream);
  * budget_ns of device time (%globaltimer) has passed since the launch began,
  * checked between proposals -- no warp idles behind a slow chain. */
 int ps_mcmc_run_budget(ps_mcmc *m, int max_proposals, uint64_t budget_ns, void *stream);
+/* Delta evaluation of given single-op changes on resident strategies: the
+ * B200 form of update_task_graph + delta_simulate (reference taskgraph.py:309-418,
+ * simulate.py:120-210; SURVEY 8b "ps_delta_batch").  The handle's chains hold
+ * the current strategies (ps_mcmc_create's initial ones, or the last committed
+ * change); for chain i, op op[i] takes local map map_local[i] and the devices
+ * assign[i * assign_stride + k], k < that map's task count.  The changed strategy
+ * is simulated from the chain's last snapshot before the change's first
+ * dependent round (bit-identical to a full simulation) and its makespan written
+ * to makespan_out[i], with status_out[i] = PS_STATUS_*.  commit[i] != 0 (or
+ * commit == NULL) keeps the change -- the chain's strategy, cost and snapshots
+ * move to it -- else the previous strategy is restored.  op[i] < 0 leaves chain
+ * i alone (makespan 0).  A chain whose change fails (no route) stays failed.
+ * The first call on a handle also scores the initial strategies.  flags:
+ * PS_HOST_PTRS (arguments checked, synchronous) or PS_DEVICE_PTRS (asynchronous
+ * on `stream`, unchecked). */
+int ps_delta_batch(ps_mcmc *m, const int32_t *op, const int32_t *map_local, const uint8_t *assign,
+                   int assign_stride, const uint8_t *commit, double *makespan_out, int32_t *status_out,
+                   int flags, void *stream);
 int ps_mcmc_read(ps_mcmc *m, ps_chain_summary *summary, int32_t *best_map, uint8_t *best_assign,
                  double *trace_cand, uint8_t *trace_ok);
 /* Number of chains, and their live (current) strategies. */

@@ -128,6 +128,8 @@ class Oracle:
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_void_p, ctypes.c_int]
         L.orc_rng_words.argtypes = [ctypes.c_int, ctypes.c_ulonglong, ctypes.c_int, ctypes.c_void_p]
+        L.orc_set_deadline.argtypes = [ctypes.c_double]
+        L.orc_set_deadline.restype = None
 
     def simulate(self, g, topo, profile, mode, strategy, cap=1 << 26) -> dict:
         """Full build + simulate of one strategy.  Returns makespan, counts and
@@ -174,8 +176,10 @@ class Oracle:
         return out
 
     def mcmc(self, g, topo, profile, mode, initial, seeds, max_proposals, max_degree,
-             rng_mode="philox", beta=None, threads=1) -> dict:
-        """polish=False MCMC, one chain per (initial strategy, seed)."""
+             rng_mode="philox", beta=None, threads=1, deadline_s=None) -> dict:
+        """polish=False MCMC, one chain per (initial strategy, seed).  ``deadline_s``
+        (bounded baseline samples only) stops every chain between proposals once
+        that much wall time has passed; summary[:, 2] says how far each got."""
         n = len(initial)
         nops = len(g.ops)
         maxsize = max(max(c.size() for c in s.configs.values()) for s in initial)
@@ -187,10 +191,12 @@ class Oracle:
         ok = np.zeros((n, max(1, max_proposals)), dtype=np.uint8)
         bdeg = np.zeros((n, nops, 5), dtype=np.int32)
         basg = np.full((n, nops, maxsize), -1, dtype=np.int32)
+        self.lib.orc_set_deadline(float(deadline_s or 0.0))
         rc = self.lib.orc_mcmc(problem_text(g, topo, profile, mode).encode(), text.encode(), max_proposals,
                                max_degree, 1 if rng_mode == "philox" else 0, beta is not None,
                                float(beta or 0.0), threads, summary.ctypes.data, cand.ctypes.data,
                                ok.ctypes.data, bdeg.ctypes.data, basg.ctypes.data, maxsize)
+        self.lib.orc_set_deadline(0.0)
         assert rc == 0, rc
         return {"summary": summary, "cand": cand, "ok": ok, "best_deg": bdeg, "best_asg": basg}
 

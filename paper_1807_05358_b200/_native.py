@@ -21,7 +21,7 @@ PS_OK, PS_ERR_INVALID, PS_ERR_NO_ROUTE, PS_ERR_CYCLE, PS_ERR_CAPACITY, PS_ERR_CU
 PS_STATUS_OK, PS_STATUS_NO_ROUTE, PS_STATUS_CAPACITY, PS_STATUS_STOPPED = 0, 2, 4, 9
 PS_HOST_PTRS, PS_DEVICE_PTRS = 0, 1
 PS_RNG_PHILOX, PS_RNG_MT19937 = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 c_int_p = ctypes.POINTER(ctypes.c_int32)
 c_i64_p = ctypes.POINTER(ctypes.c_int64)
@@ -124,6 +124,7 @@ def lib():
     L.ps_mcmc_run.argtypes = [vp, ctypes.c_int, vp]
     L.ps_mcmc_run_budget.argtypes = [vp, ctypes.c_int, ctypes.c_uint64, vp]
     L.ps_mcmc_read.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.ps_delta_batch.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, ctypes.c_int, vp]
     L.ps_mcmc_stop.argtypes = [vp, vp]
     L.ps_mcmc_chains.argtypes = [vp]
     L.ps_mcmc_read_state.argtypes = [vp, vp, vp]

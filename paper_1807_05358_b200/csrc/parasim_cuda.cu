@@ -1936,12 +1936,24 @@ __device__ inline void delta_commit(DeltaCtx *dc, int j, int lane) {
   __syncwarp();
 }
 
+// Given single-op changes (ps_delta_batch): chain i's op[i] takes local map
+// map[i] and devices asg[i * stride + k]; commit[i] keeps it (else rolled back);
+// the new makespan / status go to mk[i] / status[i].  op == nullptr: the chains
+// draw their own proposals (MCMC).
+struct Given {
+  const int *op, *map;
+  const unsigned char *asg, *commit;
+  int stride;
+  double *mk;
+  int *status;
+};
+
 template <int S>
 __global__ void __launch_bounds__(256, 1)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
-       DeltaBufs db) {
+       DeltaBufs db, Given gv) {
   constexpr bool DELTA = (S & SIM_SNAP) != 0;
   extern __shared__ __align__(16) char smem[];
   int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -1958,6 +1970,13 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   int *gmapl = maps + (size_t)chain * P.n_ops;
   unsigned char *gasg = asgs + (size_t)chain * P.n_slots;
   ChainState cs = st[chain];
+  if (gv.op) {
+    if (gv.op[chain] < 0) return;  // no change for this chain
+    if (cs.status != PS_STATUS_OK) {
+      if (lane == 0) { gv.mk[chain] = cs.cost; gv.status[chain] = cs.status; }
+      return;
+    }
+  }
   if (cs.status != PS_STATUS_OK) return;
   if (DELTA) {
     if (lane == 0) w.dc->ch = db.cd[chain];
@@ -2003,8 +2022,9 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
         if (spent + mean >= budget_ns) break;
       }
       // _propose_change (search.py:101-115): op, degree map, one device per task
-      o = (int)rng.below((unsigned)P.n_ops);
-      m = (int)rng.below((unsigned)P.op_nmaps_enum[o]);
+      // (or the caller's change: update_task_graph's op and config)
+      o = gv.op ? gv.op[chain] : (int)rng.below((unsigned)P.n_ops);
+      m = gv.op ? gv.map[chain] : (int)rng.below((unsigned)P.op_nmaps_enum[o]);
       cs.last_op = o;
       int g = T.op_map_off[o] + m;
       int size = P.map_size[g];
@@ -2015,7 +2035,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
       for (int i = lane; i < old_size; i += 32) w.oldasg[i] = w.asg[base + i];
       __syncwarp();
       for (int k = 0; k < size; ++k) {
-        unsigned dv = rng.below((unsigned)P.n_dev);
+        unsigned dv = gv.op ? gv.asg[(size_t)chain * gv.stride + k] : rng.below((unsigned)P.n_dev);
         same = same && (k < old_size && w.oldasg[k] == (unsigned char)dv);
         __syncwarp();
         if (lane == 0) w.asg[base + k] = (unsigned char)dv;
@@ -2062,6 +2082,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
       }
       if (so.status != PS_STATUS_OK) {
         cs.status = so.status; cs.err_a = so.err_a; cs.err_b = so.err_b;
+        if (gv.op && lane == 0) { gv.mk[chain] = __longlong_as_double(0x7ff0000000000000ll); gv.status[chain] = so.status; }
         if (it < 0) {
           cs.started = 1;
           cs.initial = cs.best = cs.cost = __longlong_as_double(0x7ff0000000000000ll);
@@ -2084,7 +2105,10 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
     }
     long long idx = cs.proposals++;
     bool ok;
-    if (cand <= cs.cost) ok = true;
+    if (gv.op) {
+      ok = gv.commit ? gv.commit[chain] != 0 : true;
+      if (lane == 0) { gv.mk[chain] = cand; gv.status[chain] = PS_STATUS_OK; }
+    } else if (cand <= cs.cost) ok = true;
     else {
       double pr = exp(__dmul_rn(cs.beta, __dsub_rn(cs.cost, cand)));
       ok = pr >= 1.0 ? true : rng.random() < pr;
@@ -2199,6 +2223,7 @@ struct ps_problem {
   } spare;
   size_t io_cap = 0;
   long long device_bytes = 0;
+  std::vector<int> h_map_off, h_map_size;  // host copies: argument checks of ps_delta_batch
 };
 
 struct ps_mcmc {
@@ -2217,6 +2242,8 @@ struct ps_mcmc {
   int *d_bestc;
   int cap_n;  // chains the buffers above were sized for
   DeltaBufs db;  // delta-evaluation state (db.cd == nullptr: every proposal simulates from scratch)
+  char *given = nullptr;  // ps_delta_batch staging (host-pointer calls)
+  size_t given_bytes = 0;
 };
 
 static int ensure_io(ps_problem *pr, size_t n) {
@@ -2273,6 +2300,8 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
   P.n_queues = d->n_devices + d->n_links;
   P.cap = d->ready_capacity > 0 ? d->ready_capacity : 128;
   P.mult = d->backward_multiplier;
+  pr->h_map_off.assign(d->op_map_off, d->op_map_off + P.n_ops + 1);
+  pr->h_map_size.assign(d->map_size, d->map_size + P.n_maps);
   std::vector<void *> &ow = pr->owned;
   int n_combos = 0;
   n_combos = d->combo_off[d->n_pairs];
@@ -2807,7 +2836,7 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
   return PS_OK;
 }
 
-static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, void *stream) {
+static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, void *stream, Given gv = Given{}) {
   if (!m || proposals < 0) return fail(PS_ERR_INVALID, "bad arguments");
   ps_problem *pr = m->prob;
   CK(cudaSetDevice(pr->device));
@@ -2821,7 +2850,7 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,
-      m->params.record_trace ? m->params.trace_capacity : 0, m->scratch, budget_ns, m->db);
+      m->params.record_trace && !gv.op ? m->params.trace_capacity : 0, m->scratch, budget_ns, m->db, gv);
   CK(cudaGetLastError());
   return PS_OK;
 }
@@ -2830,6 +2859,60 @@ int ps_mcmc_run(ps_mcmc *m, int proposals, void *stream) { return mcmc_launch(m,
 
 int ps_mcmc_run_budget(ps_mcmc *m, int max_proposals, uint64_t budget_ns, void *stream) {
   return mcmc_launch(m, max_proposals, (unsigned long long)budget_ns, stream);
+}
+
+int ps_delta_batch(ps_mcmc *m, const int32_t *op, const int32_t *map_local, const uint8_t *assign, int assign_stride,
+                   const uint8_t *commit, double *makespan_out, int32_t *status_out, int flags, void *stream) {
+  if (!m || !op || !map_local || !assign || assign_stride <= 0 || !makespan_out || !status_out)
+    return fail(PS_ERR_INVALID, "bad arguments");
+  ps_problem *pr = m->prob;
+  const DevProb &P = pr->P;
+  CK(cudaSetDevice(pr->device));
+  const int n = m->n;
+  Given gv{};
+  if (flags == PS_DEVICE_PTRS) {
+    gv = Given{op, map_local, assign, commit, assign_stride, makespan_out, status_out};
+    return mcmc_launch(m, 1, 0ull, stream, gv);
+  }
+  // host arguments: validate, stage in the handle's buffers, launch, read back
+  for (int i = 0; i < n; ++i) {
+    if (op[i] < 0) continue;
+    const int nm = op[i] < P.n_ops ? pr->h_map_off[op[i] + 1] - pr->h_map_off[op[i]] : 0;
+    if (op[i] >= P.n_ops || map_local[i] < 0 || map_local[i] >= nm)
+      return fail(PS_ERR_INVALID, "op or map index out of range");
+    const int size = pr->h_map_size[pr->h_map_off[op[i]] + map_local[i]];
+    if (size > assign_stride) return fail(PS_ERR_INVALID, "assign_stride is smaller than the map's task count");
+    for (int k = 0; k < size; ++k)
+      if (assign[(size_t)i * assign_stride + k] >= P.n_dev) return fail(PS_ERR_INVALID, "device index out of range");
+  }
+  size_t need = (size_t)n * (4 + 4 + 1 + 8 + 4) + (size_t)n * assign_stride + 64;
+  if (need > m->given_bytes) {
+    cudaFree(m->given);
+    m->given = nullptr;
+    CK(cudaMalloc(&m->given, need));
+    m->given_bytes = need;
+  }
+  char *b = m->given;
+  double *dmk = (double *)b; b += 8 * (size_t)n;
+  int *dop = (int *)b; b += 4 * (size_t)n;
+  int *dmap = (int *)b; b += 4 * (size_t)n;
+  int *dst = (int *)b; b += 4 * (size_t)n;
+  unsigned char *dcm = (unsigned char *)b; b += n;
+  unsigned char *dasg = (unsigned char *)b;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(dop, op, 4 * (size_t)n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dmap, map_local, 4 * (size_t)n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dasg, assign, (size_t)n * assign_stride, cudaMemcpyHostToDevice, s));
+  if (commit) CK(cudaMemcpyAsync(dcm, commit, (size_t)n, cudaMemcpyHostToDevice, s));
+  gv = Given{dop, dmap, dasg, commit ? dcm : nullptr, assign_stride, dmk, dst};
+  int rc = mcmc_launch(m, 1, 0ull, stream, gv);
+  if (rc != PS_OK) return rc;
+  CK(cudaMemcpyAsync(makespan_out, dmk, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(status_out, dst, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i)
+    if (op[i] < 0) { makespan_out[i] = 0.0; status_out[i] = PS_STATUS_OK; }
+  return PS_OK;
 }
 
 int ps_mcmc_read(ps_mcmc *m, ps_chain_summary *summary, int32_t *best_map, uint8_t *best_assign, double *trace_cand,
@@ -2961,7 +3044,7 @@ void ps_mcmc_destroy(ps_mcmc *m) {
     cudaFree(m->maps); cudaFree(m->best_maps); cudaFree(m->asgs); cudaFree(m->best_asgs); cudaFree(m->st);
     cudaFree(m->d_best); cudaFree(m->d_bestc);
   }
-  cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok);
+  cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok); cudaFree(m->given);
   cudaFree(m->db.dbg); cudaFree(m->db.cd); cudaFree(m->db.snaps); cudaFree(m->db.frb); cudaFree(m->db.indeg);
   if (m->scratch) {  // keep the largest chain scratch for the problem's next handle
     if (m->scratch_bytes >= m->prob->mcmc_scratch_bytes) {

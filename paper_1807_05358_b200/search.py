@@ -32,6 +32,7 @@ from .graph import DeviceTopology, OperatorGraph
 from .lowering import MODE_FORWARD, degree_tuple, lower
 from .partition import (ParallelizationConfig, ParallelizationStrategy, data_parallel_strategy,
                         enumerate_configs, output_region, random_strategy)
+from .parallel import shard
 from .rng import RNG_MT19937, RNG_PHILOX, mt_state_words
 
 __all__ = [
@@ -69,6 +70,7 @@ class SearchParams:
     segment: int = 256              # proposals per kernel launch between host checks
     device: int = 0
     delta: bool = True              # checkpointed delta evaluation of proposals (same results; faster)
+    devices: list | None = None     # GPUs to shard the chains over (contiguous blocks; None: [device])
 
 
 @dataclass
@@ -127,14 +129,31 @@ def propose(strategy: ParallelizationStrategy, g: OperatorGraph, topo: DeviceTop
 # batched evaluation
 
 def evaluate_strategies(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile, strategies,
-                        mode: str = MODE_FORWARD, max_degree: int | None = None, low=None) -> np.ndarray:
-    """Makespans of many strategies in one GPU launch (ps_simulate_batch).
+                        mode: str = MODE_FORWARD, max_degree: int | None = None, low=None,
+                        devices: list | None = None) -> np.ndarray:
+    """Makespans of many strategies in one GPU launch (ps_simulate_batch), or
+    one launch per GPU of ``devices`` over contiguous blocks of the list.
     Raises like build_task_graph for the first failing strategy."""
     from .taskgraph import TaskGraph, _bind, _check_config, _raise_status
     strategies = list(strategies)
     for s in strategies:
         for oid in sorted(g.ops):
             _check_config(g, topo, oid, s.configs[oid])
+    if devices and len(devices) > 1 and len(strategies) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        parts = [list(shard(r, len(devices), len(strategies))) for r in range(len(devices))]
+        jobs = [(d, p) for d, p in zip(devices, parts) if p]
+
+        def one(job):
+            d, part = job
+            sub = [strategies[i] for i in part]
+            lw = lower(g, topo, profile, mode, max_degree=max_degree, strategies=sub, device=d)
+            return evaluate_strategies(g, topo, profile, sub, mode=mode, max_degree=max_degree, low=lw)
+
+        with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
+            return np.concatenate(list(pool.map(one, jobs)))
+    if devices and low is None:
+        low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=strategies, device=devices[0])
     if low is None or not all(low.has_maps_for(s) for s in strategies):
         low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=strategies)
     n = len(strategies)
@@ -240,15 +259,41 @@ def mcmc_search(g: OperatorGraph, topo: DeviceTopology, profile: CostProfile,
     traces: list[list] = [[] for _ in range(n)]
     best: dict[int, tuple[float, ParallelizationStrategy]] = {}
     if live:
-        low = lower(g, topo, profile, params.mode, max_degree=params.max_degree,
-                    strategies=[initial[c] for c in live], device=params.device)
-        while True:
-            summaries = [None] * n
-            traces = [[] for _ in range(n)]
-            best = {}
-            if _run_chains(low, params, initial, live, summaries, traces, best, start_err):
-                break
-            low = _regrow(low)  # some chain's ready set outgrew shared memory: rerun, same streams
+        devices = list(params.devices) if params.devices else [params.device]
+        shards = [[live[i] for i in shard(r, len(devices), len(live))] for r in range(len(devices))]
+        jobs = [(d, part) for d, part in zip(devices, shards) if part]
+
+        def run_shard(device, part):
+            # every shard lowers the same map set (all live starts), so an
+            # encoded strategy means the same thing on every GPU
+            low = lower(g, topo, profile, params.mode, max_degree=params.max_degree,
+                        strategies=[initial[c] for c in live], device=device)
+            while True:
+                summ_d: list = [None] * n
+                tr_d: list = [[] for _ in range(n)]
+                best_d: dict = {}
+                err_d: dict = {}
+                if _run_chains(low, params, initial, part, summ_d, tr_d, best_d, err_d):
+                    return summ_d, tr_d, best_d, err_d
+                low = _regrow(low)  # some chain's ready set outgrew shared memory: rerun, same streams
+
+        if len(jobs) == 1:
+            results = [run_shard(*jobs[0])]
+        else:
+            # one host thread per GPU (ctypes drops the GIL inside every call);
+            # the shards share nothing until the merge below
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
+                results = list(pool.map(lambda j: run_shard(*j), jobs))
+        summaries = [None] * n
+        traces = [[] for _ in range(n)]
+        best = {}
+        for (_, part), (summ_d, tr_d, best_d, err_d) in zip(jobs, results):
+            for ci in part:
+                summaries[ci], traces[ci] = summ_d[ci], tr_d[ci]
+                if ci in best_d:
+                    best[ci] = best_d[ci]
+            start_err.update(err_d)
     for ci, msg in start_err.items():
         if summaries[ci] is None:
             _logger.warning("chain %d failed to start: %s", ci, msg[len("error: "):])

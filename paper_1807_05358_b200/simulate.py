@@ -4,11 +4,12 @@ Scheduling contract (reference simulate.py:1-11): FIFO per device and per
 link, a task is ready when its last predecessor ends, ties on ready time break
 by origin tuple.  ``full_simulate`` and ``delta_simulate`` both run the
 warp-per-candidate replay of the reference's heap order
-(``k_simulate_batch`` / ``ps_simulate_trace``); for a strategy-backed graph a
-delta evaluation *is* a full re-evaluation of the updated strategy on the
-GPU -- the reference's own contract is that the two agree exactly
-(simulate.py:121), and the incremental bookkeeping that made delta pay on a
-CPU (heap repair, queue bisection) is what the GPU path removes.
+(``k_simulate_batch`` / ``ps_simulate_trace``); for a strategy-backed graph
+``delta_simulate`` re-simulates the updated strategy on the GPU resumed from a
+snapshot of the previous simulation taken before the changed op's first
+dependent round (``ps_delta_batch`` on a resident one-chain handle); the
+reference's contract is that delta and full agree exactly (simulate.py:121),
+and they do, bit for bit.
 ``oracle_simulate`` re-simulates the materialised task list through the
 structurally separate explicit-CSR kernel (``ps_simulate_explicit``).
 """
@@ -184,8 +185,19 @@ def delta_simulate(tg: TaskGraph, changed: list[int]) -> SimulationResult:
         raise SimulationError("delta_simulate requires a prior full_simulate on this graph")
     if not changed:
         if tg._low is not None:
+            if tg._makespan is None:
+                return full_simulate(tg)
             return SimulationResult(tg._makespan, tg=tg)
         return _result(tg)
+    if tg._low is not None:
+        from .taskgraph import _delta_makespan
+        if tg._mat_valid and tg._makespan is not None:
+            mk = tg._makespan
+        else:
+            mk = _delta_makespan(tg)
+            tg._makespan = mk
+        tg.simulated = True
+        return SimulationResult(mk, tg=tg)
     return full_simulate(tg)
 
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes
 import math
 import weakref
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -100,6 +101,8 @@ class TaskGraph:
         self._asg: np.ndarray | None = None
         self._mat_valid = False
         self._makespan: float | None = None
+        self._dh = None           # resident delta-evaluation handle (_DeltaHandle)
+        self._dh_pending = None   # op ranks changed since the handle's strategy (None: out of sync)
 
     # -- explicit construction (reference taskgraph.py:114-125) ----------------
     def _new_task(self, kind, device, exe_time, origin, op_id=None, task_index=0, nbytes=0.0) -> Task:
@@ -369,37 +372,179 @@ def update_task_graph(tg: TaskGraph, g: OperatorGraph, topo: DeviceTopology, op_
 
     Returns (tg, changed).  ``changed`` is empty for a no-op swap (same degree
     dict and assignment), else the ids -- in the updated graph -- of the op's
-    own tasks and of every task whose inputs or exe time changed with it.
-    Unlike the reference, ids are renumbered in fresh-build order."""
+    own tasks and of every task whose inputs, device or exe time changed with
+    it.  Unlike the reference, ids are renumbered in fresh-build order.
+
+    The update itself only rewrites the op's fragment of the encoded strategy
+    (one map index and that op's device bytes); ``changed`` is computed, and
+    the task objects are assembled, only when someone reads them.  On a
+    topology that is not a full mesh the updated graph is materialised at once,
+    so a missing link raises NoRouteError here, as in the reference."""
     cur = tg.strategy.configs[op_id]
     if cur.degrees == new_config.degrees and cur.assignment == new_config.assignment:
         return tg, []
     if tg._low is None:
         raise RuntimeError("update_task_graph needs a strategy-backed task graph")
     _check_config(g, topo, op_id, new_config)
-    before = {t.origin: (t.exe_time, t.device, frozenset(tg._tasks[p].origin for p in t.inputs))
-              for t in tg.tasks.values()} if tg._mat_valid else None
-    tg.strategy.configs[op_id] = ParallelizationConfig(
-        dict(new_config.degrees),
-        tuple(new_config.assignment) if new_config.assignment is not None else None)
+    old_strategy = tg.strategy.copy()
+    cfg = ParallelizationConfig(dict(new_config.degrees),
+                                tuple(new_config.assignment) if new_config.assignment is not None else None)
+    tg.strategy.configs[op_id] = cfg
     low = tg._low
-    if not low.has_maps_for(tg.strategy):
+    r = low.rank[op_id]
+    t = degree_tuple(g.ops[op_id], cfg.degrees)
+    mi = low.map_index[r].get(t)
+    if mi is None:
+        # a degree map the lowered problem lacks: lower again (union of maps)
         low = _problem_for(g, topo, tg.profile, tg.mode, tg.strategy, max_degree=low.max_degree)
-    _bind(tg, low)
-    was_simulated = tg.simulated
-    _materialize(tg)
-    tg.simulated = was_simulated
-    changed = []
-    for tid, t in tg._tasks.items():
-        if t.op_id == op_id or (t.origin[0] in ("edge", "edge_bwd", "sync") and op_id in t.origin[1:3]):
-            changed.append(tid)
+        _bind(tg, low)
+    else:
+        # patch the encoded fragment in place
+        tg._map[r] = mi
+        base = int(low.slot_off[r])
+        for k in range(math.prod(t)):
+            tg._asg[base + k] = low.dev_index[cfg.assignment[k]]
+        tg._mat_valid = False
+    tg._makespan = None
+    if tg._dh is not None and tg._dh_pending is not None and tg._dh.low is tg._low:
+        tg._dh_pending.append(r)
+    else:
+        tg._dh_pending = None
+    if not _full_mesh(low):
+        was_simulated = tg.simulated
+        _materialize(tg)  # raises NoRouteError for a missing link, like the reference's update
+        tg.simulated = was_simulated
+    return tg, ChangedTasks(tg, old_strategy, tg.strategy.copy(), op_id)
+
+
+def _full_mesh(low: Lowered) -> bool:
+    """Every device pair connected: no strategy can need a missing link."""
+    v = getattr(low, "_full_mesh", None)
+    if v is None:
+        topo = low.topology
+        ids = topo.device_ids()
+        v = all(topo.connection_between(a, b) is not None for i, a in enumerate(ids) for b in ids[i + 1:])
+        low._full_mesh = v
+    return v
+
+
+class ChangedTasks(Sequence):
+    """update_task_graph's ``changed`` list, computed on first access: the op's
+    own tasks and transfers / ring hops, plus every task whose device, exe time
+    or input origins differ between the graph before and after the change."""
+
+    __slots__ = ("_args", "_ids")
+
+    def __init__(self, tg, old_strategy, new_strategy, op_id):
+        self._args = (tg.graph, tg.topology, tg.profile, tg.mode, old_strategy, new_strategy, op_id)
+        self._ids = None
+
+    def _get(self) -> list:
+        if self._ids is None:
+            g, topo, profile, mode, old_s, new_s, op_id = self._args
+            graphs = []
+            for strat in (old_s, new_s):
+                x = TaskGraph(g, topo, strat, profile, mode)
+                _bind(x, _problem_for(g, topo, profile, mode, strat))
+                _materialize(x)
+                graphs.append(x)
+            old, new = graphs
+            before = {t.origin: (t.exe_time, t.device, frozenset(old._tasks[p].origin for p in t.inputs))
+                      for t in old._tasks.values()}
+            out = []
+            for tid, t in new._tasks.items():
+                if t.op_id == op_id or (t.origin[0] in ("edge", "edge_bwd", "sync") and op_id in t.origin[1:3]):
+                    out.append(tid)
+                    continue
+                prev = before.get(t.origin)
+                if prev is None or prev != (t.exe_time, t.device, frozenset(new._tasks[p].origin for p in t.inputs)):
+                    out.append(tid)
+            self._ids = sorted(out)
+            self._args = None
+        return self._ids
+
+    def __bool__(self):
+        return True  # the changed op always has at least one task
+
+    def __len__(self):
+        return len(self._get())
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __eq__(self, other):
+        return list(self) == list(other) if isinstance(other, (list, tuple, Sequence)) else NotImplemented
+
+    def __repr__(self):
+        return repr(self._get())
+
+
+class _DeltaHandle:
+    """A one-chain ps_mcmc handle with delta evaluation on: it holds the
+    strategy the task graph was last delta-simulated with, and that
+    simulation's snapshots, so the next single-op change resumes mid-timeline
+    (ps_delta_batch)."""
+
+    def __init__(self, low: Lowered, m: np.ndarray, a: np.ndarray):
+        L = nat.lib()
+        self.low = low
+        self.h = ctypes.c_void_p()
+        mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0, 1)
+        seeds = np.zeros(1, dtype=np.uint64)
+        nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), 1, nat.ptr(m), nat.ptr(a), nat.ptr(seeds), None,
+                                   ctypes.byref(self.h)), "ps_mcmc_create")
+        weakref.finalize(self, L.ps_mcmc_destroy, self.h, low)  # (low: keeps the problem alive until then)
+        nat.check(L.ps_mcmc_run(self.h, 0, None), "ps_mcmc_run")  # scores (and snapshots) the strategy
+        summ = (nat.PsChainSummary * 1)()
+        nat.check(L.ps_mcmc_read(self.h, summ, None, None, None, None), "ps_mcmc_read")
+        self.cost, self.status = float(summ[0].cost), int(summ[0].status)
+        self._op = np.zeros(1, dtype=np.int32)
+        self._mi = np.zeros(1, dtype=np.int32)
+        self._mk = np.zeros(1, dtype=np.float64)
+        self._st = np.zeros(1, dtype=np.int32)
+
+    def change(self, r: int, mi: int, devices: np.ndarray):
+        """Commit op rank r := (map mi, devices); returns (makespan, status)."""
+        self._op[0], self._mi[0] = r, mi
+        a = np.ascontiguousarray(devices, dtype=np.uint8)
+        nat.check(nat.lib().ps_delta_batch(self.h, nat.ptr(self._op), nat.ptr(self._mi), nat.ptr(a), max(1, a.size),
+                                           None, nat.ptr(self._mk), nat.ptr(self._st), nat.PS_HOST_PTRS, None),
+                  "ps_delta_batch")
+        self.cost, self.status = float(self._mk[0]), int(self._st[0])
+        return self.cost, self.status
+
+
+def _delta_makespan(tg: TaskGraph) -> float:
+    """Makespan of the updated strategy by delta evaluation on the task graph's
+    resident handle (created -- one from-scratch scoring -- on first use)."""
+    for _ in range(4):
+        low = tg._low
+        dh, pend = tg._dh, tg._dh_pending
+        if dh is not None and dh.low is low and pend is not None and dh.status == nat.PS_STATUS_OK \
+                and len(set(pend)) <= 4:
+            st = nat.PS_STATUS_OK
+            mk = dh.cost
+            for r in dict.fromkeys(pend):  # each changed op once, in update order
+                size = int(low.arrays["map_size"][low.arrays["op_map_off"][r] + int(tg._map[r])])
+                base = int(low.slot_off[r])
+                mk, st = dh.change(r, int(tg._map[r]), tg._asg[base:base + size])
+                if st != nat.PS_STATUS_OK:
+                    break
+        else:
+            dh = _DeltaHandle(low, tg._map, tg._asg)
+            mk, st = dh.cost, dh.status
+        if st == nat.PS_STATUS_OK:
+            tg._dh, tg._dh_pending = dh, []
+            return mk
+        tg._dh, tg._dh_pending = None, None
+        if st == nat.PS_STATUS_CAPACITY:
+            _grow(tg)  # a ready set outgrew shared memory: 4x capacity, new handle
             continue
-        if before is not None:
-            prev = before.get(t.origin)
-            if prev is None or prev != (t.exe_time, t.device,
-                                        frozenset(tg._tasks[p].origin for p in t.inputs)):
-                changed.append(tid)
-    return tg, sorted(changed)
+        _raise_status(tg, st)
+    raise RuntimeError("delta evaluation did not converge on a ready-set capacity")
 
 
 def _creation_key(low: Lowered, topo_pos: dict, pair_pos: dict, origin: tuple):

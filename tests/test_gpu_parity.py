@@ -518,3 +518,162 @@ def test_delta_evaluation_on_large_and_heterogeneous_problems(oracle):
             assert [(s.initial_cost, s.best_cost, s.proposals, s.accepted) for s in a] == \
                 [tuple(r[:4]) for r in ref["summary"]], mode
             assert np.array_equal(at, ref["cand"])
+
+
+@pytest.mark.parametrize("mode", [ps.MODE_FULL, ps.MODE_FORWARD])
+def test_delta_batch_abi_matches_full_evaluation(oracle, mode):
+    """ps_delta_batch (the C-ABI form of update_task_graph + delta_simulate):
+    per chain, 40 rounds of a given single-op change, committed or rolled back
+    at random; every makespan equals a from-scratch batch evaluation of the
+    changed strategy, the chains' live strategies follow the commits, and a
+    sample matches the oracle."""
+    import ctypes
+    from paper_1807_05358_b200 import _native as nat
+    from paper_1807_05358_b200.lowering import lower
+    g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
+    prof = ps.CostProfile()
+    C = 64
+    init = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, md, list(range(1, C)))
+    low = lower(g, topo, prof, mode, max_degree=md, strategies=init)
+    maps = np.zeros((C, low.n_ops), dtype=np.int32)
+    asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+    for i, s in enumerate(init):
+        low.encode(s, maps[i], asg[i])
+    L = nat.lib()
+    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 0, 0, 1)
+    h = ctypes.c_void_p()
+    sd = np.zeros(C, dtype=np.uint64)
+    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(sd), None,
+                               ctypes.byref(h)), "ps_mcmc_create")
+    rng = np.random.default_rng(3)
+    nmaps = low.arrays["op_nmaps_enum"]
+    stride = int(max(low.arrays["map_size"]))
+    checked = []
+    try:
+        for step in range(40):
+            op = rng.integers(0, low.n_ops, C).astype(np.int32)
+            op[rng.random(C) < 0.1] = -1  # some chains sit this round out
+            mi = np.array([rng.integers(0, nmaps[o]) if o >= 0 else 0 for o in op], dtype=np.int32)
+            dv = rng.integers(0, topo.device_ids().__len__(), (C, stride)).astype(np.uint8)
+            commit = (rng.random(C) < 0.5).astype(np.uint8)
+            mk = np.zeros(C)
+            st = np.zeros(C, dtype=np.int32)
+            nat.check(L.ps_delta_batch(h, nat.ptr(op), nat.ptr(mi), nat.ptr(dv), stride, nat.ptr(commit), nat.ptr(mk),
+                                       nat.ptr(st), nat.PS_HOST_PTRS, None), "ps_delta_batch")
+            assert (st == nat.PS_STATUS_OK).all()
+            # the changed strategies, scored from scratch
+            cm, ca = maps.copy(), asg.copy()
+            for i in range(C):
+                if op[i] < 0:
+                    continue
+                r = int(op[i])
+                cm[i, r] = mi[i]
+                size = int(low.arrays["map_size"][low.arrays["op_map_off"][r] + mi[i]])
+                base = int(low.slot_off[r])
+                ca[i, base:base + size] = dv[i, :size]
+            live = op >= 0
+            fresh = np.zeros(C)
+            fst = np.zeros(C, dtype=np.int32)
+            nat.check(L.ps_simulate_batch(low.handle(), nat.ptr(cm), nat.ptr(ca), C, nat.ptr(fresh), nat.ptr(fst),
+                                          nat.PS_HOST_PTRS, None), "ps_simulate_batch")
+            assert np.array_equal(mk[live], fresh[live]), step
+            keep = live & (commit != 0)
+            maps[keep], asg[keep] = cm[keep], ca[keep]
+            if step % 10 == 9:
+                checked.append((low.decode(cm[1], ca[1]), float(mk[1])))
+        sm = np.zeros_like(maps)
+        sa = np.zeros_like(asg)
+        nat.check(L.ps_mcmc_read_state(h, nat.ptr(sm), nat.ptr(sa)), "ps_mcmc_read_state")
+        assert np.array_equal(sm, maps)
+        for i in range(C):  # live strategies: compare the used slots of each op
+            for r in range(low.n_ops):
+                size = int(low.arrays["map_size"][low.arrays["op_map_off"][r] + maps[i, r]])
+                base = int(low.slot_off[r])
+                assert np.array_equal(sa[i, base:base + size], asg[i, base:base + size])
+        summ = (nat.PsChainSummary * C)()
+        nat.check(L.ps_mcmc_read(h, summ, None, None, None, None), "ps_mcmc_read")
+        assert sum(s.rounds_reused for s in summ) > 0
+    finally:
+        L.ps_mcmc_destroy(h)
+    want = oracle.makespans(g, topo, prof, mode, [s for s, _ in checked])
+    assert [m for _, m in checked] == list(want)
+
+
+def test_api_delta_resumes_on_the_resident_handle(oracle):
+    """update_task_graph + delta_simulate through the drop-in API: the task
+    graph keeps a resident delta handle, ``changed`` is computed lazily and
+    equals the eager definition, and results match fresh builds."""
+    from paper_1807_05358_b200.taskgraph import ChangedTasks
+    g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
+    prof = ps.CostProfile()
+    rng = random.Random(11)
+    tg = ps.build_task_graph(g, topo, ps.random_strategy(g, topo, md, 1), prof, ps.MODE_FULL)
+    ps.full_simulate(tg)
+    for step in range(30):
+        op_id = rng.choice(sorted(g.ops))
+        cfg = rng.choice(ps.enumerate_configs(g.ops[op_id], topo, md))
+        asg = tuple(rng.choice(topo.device_ids()) for _ in range(cfg.size()))
+        before = tg.strategy.copy()
+        _, changed = ps.update_task_graph(tg, g, topo, op_id, ps.ParallelizationConfig(dict(cfg.degrees), asg))
+        res = ps.delta_simulate(tg, changed)
+        assert tg._dh is not None and tg._dh_pending == []
+        fresh = ps.build_task_graph(g, topo, tg.strategy, prof, ps.MODE_FULL)
+        assert res.makespan == ps.full_simulate(fresh).makespan
+        if step % 10 == 0 and isinstance(changed, ChangedTasks):
+            old = ps.build_task_graph(g, topo, before, prof, ps.MODE_FULL)
+            prev = {t.origin: (t.exe_time, t.device, frozenset(old.tasks[p].origin for p in t.inputs))
+                    for t in old.tasks.values()}
+            want = sorted(tid for tid, t in fresh.tasks.items()
+                          if t.op_id == op_id or (t.origin[0] in ("edge", "edge_bwd", "sync") and op_id in t.origin[1:3])
+                          or prev.get(t.origin) != (t.exe_time, t.device,
+                                                    frozenset(fresh.tasks[p].origin for p in t.inputs)))
+            assert list(changed) == want
+            assert ps.timeline_table(tg) == ps.timeline_table(fresh)
+    assert tg._dh is not None
+    assert oracle.simulate(g, topo, prof, ps.MODE_FULL, tg.strategy)["makespan"] == res.makespan
+
+
+@pytest.mark.parametrize("budget", [None, 0.5])
+def test_sharded_search_equals_single_gpu_search(budget):
+    """mcmc_search(devices=[...]): chains split into contiguous shards, one host
+    thread and problem copy per GPU (here two shards on GPU 0), merged with the
+    reference's earliest-chain rule (search.py:256).  With a proposal limit the
+    report is byte-identical to the one-GPU run of the same chains; time-boxed,
+    every chain's trajectory is an exact prefix of the same stream."""
+    g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
+    prof = ps.CostProfile()
+    C = 48
+    init = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, md, list(range(1, C)))
+    kw = dict(seed=3, max_degree=md, mode=ps.MODE_FULL, initial=init, polish=False, rng="philox")
+    if budget is None:
+        kw["max_proposals"] = 60
+    else:
+        kw["budget_seconds"] = budget
+    one = ps.mcmc_search(g, topo, prof, ps.SearchParams(**kw))
+    two = ps.mcmc_search(g, topo, prof, ps.SearchParams(devices=[0, 0], **kw))
+    if budget is None:
+        assert ps.formats.report_to_json(one) == ps.formats.report_to_json(two)
+        # a three-way split with an uneven last shard
+        three = ps.mcmc_search(g, topo, prof, ps.SearchParams(devices=[0, 0, 0], **kw))
+        assert ps.formats.report_to_json(one) == ps.formats.report_to_json(three)
+    else:
+        for a, b in zip(one.chains, two.chains):
+            assert a.initial_cost == b.initial_cost and a.beta == b.beta
+        # chain-by-chain: the shorter run's trace is a prefix of the longer one's
+        off_a = off_b = 0
+        for a, b in zip(one.chains, two.chains):
+            ta = [c for _, c, _ in one.trace[off_a:off_a + a.proposals]]
+            tb = [c for _, c, _ in two.trace[off_b:off_b + b.proposals]]
+            k = min(len(ta), len(tb))
+            assert ta[:k] == tb[:k]
+            off_a += a.proposals
+            off_b += b.proposals
+
+
+def test_sharded_evaluation_equals_one_launch():
+    g, topo, md = ps.inception_v3(), ps.multi_node_topology(4, 4), 4
+    prof = ps.CostProfile()
+    strategies = ps.random_strategies(g, topo, md, list(range(37)))
+    a = ps.evaluate_strategies(g, topo, prof, strategies, mode=ps.MODE_FULL, max_degree=md)
+    b = ps.evaluate_strategies(g, topo, prof, strategies, mode=ps.MODE_FULL, max_degree=md, devices=[0, 0, 0])
+    assert list(a) == list(b)
