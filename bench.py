@@ -221,7 +221,7 @@ def run_reference(args):
     vals = []
     for i in range(args.warmup + args.steps):
         # warm-up steps are short (1 s); timed steps are wall-clock-bounded samples
-        secs = 1.0 if i < args.warmup else max(2.0, args.cpu_seconds / 4)
+        secs = 1.0 if i < args.warmup else max(2.0, args.cpu_seconds / 2)
         res = cpu_baseline(g, topo, prof, args.mode, md, init, seeds, secs, threads)
         if i >= args.warmup:
             vals.append(res["value"])

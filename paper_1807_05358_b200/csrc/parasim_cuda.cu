@@ -358,6 +358,14 @@ struct Lay {  // sizes shared by host and device
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// per-warp phase counters of -DPS_PHASES builds (16 bytes otherwise)
+#ifdef PS_PHASES
+#define PH_N 24
+#else
+#define PH_N 2
+#endif
+#define PH_BYTES (PH_N * 8)
+
 // ---------------------------------------------------------------- delta
 // Checkpointed ("delta") evaluation, the B200 form of the reference's
 // update_task_graph + delta_simulate (taskgraph.py:309-418, simulate.py:120-210).
@@ -466,7 +474,7 @@ __host__ __device__ inline size_t warp_bytes_of(const DevProb &P, int SC, int GC
   b += al16(8 * (size_t)SC) + al16(2 * (size_t)SC) + al16((size_t)SC / 2);  // counters: ready, remaining, shard id
   b += al16(8 * (size_t)GC);                         // ring device masks
   b += al16(4 * (size_t)RC) * 2;                     // staged row / column offsets
-  b += 256 + 128 + 16;                               // proposal staging, phase counters
+  b += 256 + PH_BYTES + 16;                          // proposal staging, phase counters
   b += al16(sizeof(DeltaCtx));                       // delta context
   b += al16(2 * (size_t)P.n_ops);                    // delta: ops seen running
   return b;
@@ -575,7 +583,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.srow = (int *)take(4 * L.RC);
   w.scol = (int *)take(4 * L.RC);
   w.oldasg = (unsigned char *)take(256);
-  w.ph = (unsigned long long *)take(128);
+  w.ph = (unsigned long long *)take(PH_BYTES);
   w.dc = (DeltaCtx *)take(sizeof(DeltaCtx));
   w.ran = (unsigned char *)take(2 * P.n_ops);
   w.rcap = P.cap;
@@ -886,7 +894,7 @@ __device__ int g_tc_sim;
 #define TC(i)
 #endif
 #ifdef PS_PHASES
-__device__ unsigned long long g_phase[16];
+__device__ unsigned long long g_phase[PH_N];
 #define PH_T(v) long long v = clock64()
 #define PH_ADD(i, t0) do { if (lane == 0) w.ph[i] += (unsigned long long)(clock64() - (t0)); } while (0)
 #define PH_CNT(i, x) do { if (lane == 0) w.ph[i] += (unsigned long long)(x); } while (0)
@@ -1287,6 +1295,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       TC(6);
       PH_ADD(15, t_cl);
     } else {
+      PH_T(t_slow);
+      PH_CNT(16, 1);
+      PH_CNT(17, n);
       if (lane == 0) w.flags[0] = 1;
       dirty = true;
       // ---- scan 1: minimum key and LB = min(ready + exe)
@@ -1378,6 +1389,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       mine = lane < nw;
       w.wlane[lane] = lane;
+      PH_ADD(19, t_slow);
+      PH_CNT(18, nw);
     }
     // ---- run the winners: per queue in (ready, origin) order
 #pragma unroll 1
@@ -2000,7 +2013,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   unsigned char *basg = best_asgs + (size_t)chain * P.n_slots;
   unsigned long long t0 = globaltimer_ns();
 #ifdef PS_PHASES
-  for (int i = lane; i < 16; i += 32) w.ph[i] = 0;
+  for (int i = lane; i < PH_N; i += 32) w.ph[i] = 0;
   __syncwarp();
 #endif
   PH_T(t_loop);
@@ -2139,7 +2152,7 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   PH_CNT(7, n_it);
 #ifdef PS_PHASES
   __syncwarp();
-  if (lane < 16) atomicAdd(&g_phase[lane], w.ph[lane]);
+  if (lane < PH_N) atomicAdd(&g_phase[lane], w.ph[lane]);
 #endif
   for (int i = lane; i < P.n_ops; i += 32) gmapl[i] = w.mapl[i];
   if (!lay.asg_global)
@@ -3000,9 +3013,9 @@ int ps_debug_tcyc(long long *out) {
 int ps_debug_phases(unsigned long long *out, int reset) {
 #ifdef PS_PHASES
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16));
+  CK(cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * PH_N));
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[PH_N] = {0};
     CK(cudaMemcpyToSymbol(g_phase, z, sizeof z));
   }
   return PS_OK;

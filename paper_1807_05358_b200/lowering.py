@@ -31,6 +31,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
+from .cost import cost_key_for
 from .graph import DeviceTopology, OperatorGraph, parallelizable_dims
 from .partition import ParallelizationConfig, enumerate_configs, grid_of, need_descriptors, output_region
 
@@ -197,9 +198,13 @@ class Lowered:
 
 
 def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree: int | None = None,
-          strategies=(), ready_capacity: int = 128, device: int = 0) -> Lowered:
+          strategies=(), ready_capacity: int = 128, device: int = 0, quiet_extra: bool = False) -> Lowered:
     """Flatten a problem.  ``max_degree`` adds every enumerate_configs map (the
-    MCMC proposal space); ``strategies`` adds the maps those strategies use."""
+    MCMC proposal space); ``strategies`` adds the maps those strategies use.
+    ``quiet_extra``: maps no given strategy uses are priced without inserting
+    into ``profile.entries`` (a build then leaves the profile as the reference's
+    build of those strategies would; update_task_graph inserts a map's entry
+    when a strategy first uses it)."""
     if mode not in (MODE_FORWARD, MODE_FULL):
         raise ValueError(f"unknown mode {mode!r}")
     ops = sorted(g.ops)
@@ -239,6 +244,7 @@ def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree
     maps: list[list[tuple[int, ...]]] = []
     map_index: list[dict] = []
     n_enum: list[int] = []
+    used: list[set] = []  # per op: the maps some given strategy uses
     for oid in ops:
         op = g.ops[oid]
         lst = []
@@ -247,6 +253,8 @@ def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree
         n_enum.append(len(lst))
         idx = {t: i for i, t in enumerate(lst)}
         seen = {}  # id(degrees dict) -> tuple: batched strategies share their dicts
+        used_r = set()
+        used.append(used_r)
         for s in strategies:
             cfg = s.configs.get(oid)
             if cfg is None:
@@ -254,6 +262,7 @@ def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree
             t = seen.get(id(cfg.degrees))
             if t is None:
                 t = seen[id(cfg.degrees)] = degree_tuple(op, cfg.degrees)
+                used_r.add(t)
             if t not in idx:
                 grid_of(op, ParallelizationConfig(dict(zip(op.output_shape.names(), t))))  # divisibility
                 idx[t] = len(lst)
@@ -304,8 +313,15 @@ def lower(g: OperatorGraph, topo: DeviceTopology, profile, mode: str, max_degree
             max_size[r] = max(max_size[r], size)
             cfg = ParallelizationConfig(dict(zip(names, t)))
             region0 = output_region(op, cfg, 0)
+            quiet = quiet_extra and t not in used[r]
             for kname, ki in kind_index.items():
-                e = profile.task_exe_time(op, region0, dev_of_kind[kname])
+                if quiet:
+                    key = cost_key_for(op, region0, kname)
+                    e = profile.entries.get(key)
+                    if e is None:
+                        e = profile.fallback.time(op, key)
+                else:
+                    e = profile.task_exe_time(op, region0, dev_of_kind[kname])
                 if not e >= 0.0:
                     # the reference would schedule a negative (or NaN) time; its heap order
                     # is then no longer monotone in ready time, which the GPU replay assumes

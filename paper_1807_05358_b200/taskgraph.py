@@ -30,7 +30,7 @@ from . import _native as nat
 from .cost import CostProfile
 from .graph import Connection, DeviceTopology, OperatorGraph, parallelizable_dims
 from .lowering import MODE_FORWARD, MODE_FULL, Lowered, degree_tuple, lower, origin_of
-from .partition import ParallelizationConfig, ParallelizationStrategy, block_coords
+from .partition import ParallelizationConfig, ParallelizationStrategy, block_coords, output_region
 
 __all__ = [
     "MODE_FORWARD", "MODE_FULL", "Task", "TimelineEntry", "TaskGraph", "NoRouteError",
@@ -223,7 +223,11 @@ def _problem_for(g, topo, profile, mode, strategy, max_degree=None) -> Lowered:
             max_degree = low.max_degree
     else:
         strategies = [strategy]
-    low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=strategies)
+        if max_degree is None:
+            # every degree map of the reference's default proposal space (SearchParams.max_degree
+            # = 4): update_task_graph to any of them then rewrites the encoded fragment in place
+            max_degree = min(4, len(topo.devices))
+    low = lower(g, topo, profile, mode, max_degree=max_degree, strategies=strategies, quiet_extra=True)
     # lowering inserts the fallback's answers into profile.entries: fingerprint after
     _cache_put(profile, _fingerprint(g, topo, profile, mode), low, strategies[-8:])
     return low
@@ -405,6 +409,7 @@ def update_task_graph(tg: TaskGraph, g: OperatorGraph, topo: DeviceTopology, op_
         for k in range(math.prod(t)):
             tg._asg[base + k] = low.dev_index[cfg.assignment[k]]
         tg._mat_valid = False
+        _touch_profile(tg, op_id, cfg)
     tg._makespan = None
     if tg._dh is not None and tg._dh_pending is not None and tg._dh.low is tg._low:
         tg._dh_pending.append(r)
@@ -415,6 +420,25 @@ def update_task_graph(tg: TaskGraph, g: OperatorGraph, topo: DeviceTopology, op_
         _materialize(tg)  # raises NoRouteError for a missing link, like the reference's update
         tg.simulated = was_simulated
     return tg, ChangedTasks(tg, old_strategy, tg.strategy.copy(), op_id)
+
+
+def _touch_profile(tg: TaskGraph, op_id: str, cfg: ParallelizationConfig):
+    """The profile lookups the reference's update makes for the new fragment
+    (cost.py:113-121): a map first used here inserts its entry.  The lowered
+    tables already hold the same value, so the cached problem stays valid."""
+    prof, op = tg.profile, tg.graph.ops[op_id]
+    n0 = len(prof.entries)
+    region0 = output_region(op, cfg, 0)
+    kinds = {}
+    for dev in cfg.assignment[:math.prod(degree_tuple(op, cfg.degrees))]:
+        d = tg.topology.devices[dev]
+        kinds.setdefault(d.kind, d)
+    for d in kinds.values():
+        prof.task_exe_time(op, region0, d)
+    if len(prof.entries) != n0:
+        hit = _cache_get(prof)
+        if hit is not None and hit[2] is tg._low:
+            _cache_put(prof, _fingerprint(tg.graph, tg.topology, prof, tg.mode), hit[2], hit[3])
 
 
 def _full_mesh(low: Lowered) -> bool:
@@ -482,6 +506,10 @@ class ChangedTasks(Sequence):
         return repr(self._get())
 
 
+def _destroy_handle(h, _low):
+    nat.lib().ps_mcmc_destroy(h)
+
+
 class _DeltaHandle:
     """A one-chain ps_mcmc handle with delta evaluation on: it holds the
     strategy the task graph was last delta-simulated with, and that
@@ -496,7 +524,7 @@ class _DeltaHandle:
         seeds = np.zeros(1, dtype=np.uint64)
         nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), 1, nat.ptr(m), nat.ptr(a), nat.ptr(seeds), None,
                                    ctypes.byref(self.h)), "ps_mcmc_create")
-        weakref.finalize(self, L.ps_mcmc_destroy, self.h, low)  # (low: keeps the problem alive until then)
+        weakref.finalize(self, _destroy_handle, self.h, low)  # (low: keeps the problem alive until then)
         nat.check(L.ps_mcmc_run(self.h, 0, None), "ps_mcmc_run")  # scores (and snapshots) the strategy
         summ = (nat.PsChainSummary * 1)()
         nat.check(L.ps_mcmc_read(self.h, summ, None, None, None, None), "ps_mcmc_read")

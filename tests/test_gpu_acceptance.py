@@ -175,3 +175,44 @@ def test_time_boxed_search_records_its_trace_and_verifies():
                                                            max_degree=4, polish=False, segment=48))
     assert all(c.proposals == 100 and c.termination == "proposal-limit" for c in capped.chains)
     assert len(capped.trace) == 200
+
+
+def test_criterion_4_search_attains_the_proven_optimum():
+    """test_acceptance.py:145-172 on the GPU path: on instances small enough to
+    solve exactly (lenet-like, 2-step rnnlm-like, max degree 2, 4 GPUs), the
+    default two-chain search finds the exhaustive optimum in >= 9 of 10 seeds.
+    The reference gives each search 60 s; here each gets a 4000-proposal limit
+    (a fraction of a second on the GPU)."""
+    topo = ps.single_node_topology(gpus=4)
+    prof = ps.CostProfile()
+    fixtures = (
+        ("lenet-like", ps.lenet_like(batch=2, image=4, in_channels=1, conv_channels=(2, 2), fc_hidden=2, classes=2)),
+        ("rnnlm-like", ps.rnnlm_like(steps=2, layers=1, batch=2, hidden=2, vocab=2)),
+    )
+    for name, g in fixtures:
+        res = ps.exhaustive_optimal(g, topo, prof, max_degree=2, cap=1e15)
+        hits = 0
+        for seed in range(10):
+            rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=4000, seed=seed, max_degree=2,
+                                                                 mode=ps.MODE_FORWARD))
+            assert rep.best_cost >= res.cost
+            hits += rep.best_cost == res.cost
+        assert hits >= 9, (name, hits, res.cost)
+
+
+def test_criterion_6_search_beats_data_parallel_on_a_param_heavy_net():
+    """test_acceptance.py:198-224 on the GPU path: when the final dense layer
+    holds ~99% of the parameters, the found strategy beats data parallelism on
+    both makespan and transferred bytes."""
+    g = ps.lenet_like(batch=8, image=8, in_channels=2, conv_channels=(4, 8), fc_hidden=32, classes=4096)
+    dominant = max(g.ops.values(), key=lambda op: op.param_bytes)
+    assert dominant.id == "fc2"
+    assert dominant.param_bytes > 0.9 * sum(op.param_bytes for op in g.ops.values())
+    topo = ps.single_node_topology(gpus=4)
+    prof = ps.CostProfile()
+    dp = ps.full_simulate(ps.build_task_graph(g, topo, ps.data_parallel_strategy(g, topo), prof, ps.MODE_FULL))
+    rep = ps.mcmc_search(g, topo, prof, ps.SearchParams(max_proposals=4000, seed=0, max_degree=4, mode=ps.MODE_FULL))
+    best = ps.full_simulate(ps.build_task_graph(g, topo, rep.best_strategy, prof, ps.MODE_FULL))
+    assert best.makespan == rep.best_cost
+    assert best.makespan < dp.makespan
+    assert best.total_comm_bytes < dp.total_comm_bytes
