@@ -354,6 +354,7 @@ struct Lay {  // sizes shared by host and device
   int RC;  // staged row / column offset capacity
   int asg_global;  // device assignment read in place from global memory (very wide problems)
   int global_all;  // block tables and warp slices in global memory (problems too big for shared memory)
+  int hot_bytes;   // global_all: per-warp shared-memory slice for the per-round state (0: none)
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -493,6 +494,13 @@ struct W2 {
   int *flags;  // [0]: slow-path queue bids may be dirty
   int *wlane;  // [32] lane holding the k-th winner of the round
   int rcap;    // ready-set capacity in effect (shared memory, or the global overflow slice)
+  // Back ready set (global, unsorted): entries that did not fit in (or were
+  // trimmed from) the front set w.rs.  Rounds run on the front set while the
+  // back set's ready times are bounded below by the round's LB; see
+  // "two-level ready set" at warp_simulate2.  bcap == 0: no back set.
+  REnt *bq;
+  int *bmem;
+  int bcap;
   double *opmin;  // optional [n_ops]: earliest end of each op's forward tasks (exhaustive bounds)
   const TraceSink *tr;  // optional: record every task and dependency (API materialisation)
   double *cready;
@@ -587,6 +595,9 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.dc = (DeltaCtx *)take(sizeof(DeltaCtx));
   w.ran = (unsigned char *)take(2 * P.n_ops);
   w.rcap = P.cap;
+  w.bq = nullptr;
+  w.bmem = nullptr;
+  w.bcap = 0;
   w.opmin = nullptr;
   w.tr = nullptr;
 }
@@ -612,12 +623,30 @@ __host__ __device__ inline size_t gslice_bytes(const DevProb &P, const Lay &L) {
   return al16(gscratch_bytes(P.n_slots, P.n_queues)) + (L.global_all ? L.warp_bytes : 0);
 }
 
+// The per-round state -- front ready set, member list, queue clocks, flags and
+// winner lanes -- of a warp whose layout is otherwise in global memory
+// (global_all): kept in shared memory when the launch provides hot_bytes per warp.
+__host__ __device__ inline size_t hot_bytes_of(const DevProb &P) {
+  return al16(32 * (size_t)P.cap) + al16(4 * (size_t)P.cap) + al16(8 * (size_t)P.n_queues) + 16 + 128;
+}
+
+__device__ inline void carve_hot(char *base, const DevProb &P, W2 &w) {
+  char *p = base;
+  auto take = [&](size_t bytes) { char *r = p; p += al16(bytes); return r; };
+  w.rs = (REnt *)take(32 * (size_t)P.cap);
+  w.mem = (int *)take(4 * (size_t)P.cap);
+  w.qclock = (double *)take(8 * (size_t)P.n_queues);
+  w.flags = (int *)take(16);
+  w.wlane = (int *)take(128);
+}
+
 // prologue shared by the warp kernels: block tables and this warp's layout
 __device__ inline void kernel_layout(const DevProb &P, const Lay &L, char *smem, char *gslice, int wib, Tab &T,
                                      W2 &w) {
   if (L.global_all) {
     tab_from_global(P, T);
     carve_warp(gslice + al16(gscratch_bytes(P.n_slots, P.n_queues)), P, L, w);
+    if (L.hot_bytes) carve_hot(smem + (size_t)wib * L.hot_bytes, P, w);
   } else {
     carve_tab(smem, P, T);
     load_tab(P, T);
@@ -632,6 +661,11 @@ __device__ inline void bind_bids(const DevProb &P, char *gscratch, W2 &w) {
             al16((size_t)P.n_slots * 8);
   w.qready = (unsigned long long *)g;
   w.qbest = w.qready + P.n_queues;
+  // the back ready set lives in the overflow slice
+  char *b = g + al16((size_t)P.n_queues * 16);
+  w.bcap = overflow_cap(P.n_slots);
+  w.bq = (REnt *)b;
+  w.bmem = (int *)(w.bq + w.bcap);
 }
 
 // Ready set in the warp's global slice (exact overflow path for wide candidates).
@@ -642,6 +676,9 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
   w.rs = (REnt *)g;
   w.mem = (int *)(w.rs + c);
   w.rcap = c;
+  w.bq = nullptr;  // (the front set now occupies the back set's slice)
+  w.bmem = nullptr;
+  w.bcap = 0;
   return w;
 }
 
@@ -690,12 +727,49 @@ __device__ inline SimOut simulate_any(const DevProb &P, const Tab &T, const W2 &
   return o;
 }
 
+// warp-wide lexicographic min of 64-bit (hi, lo) pairs; returns winning lane
+__device__ __forceinline__ int warp_argmin128(unsigned long long hi, unsigned long long lo, int lane) {
+  unsigned cand = FULLMASK, v, mn;
+  v = (unsigned)(hi >> 32); mn = __reduce_min_sync(FULLMASK, v); cand = __ballot_sync(FULLMASK, v == mn);
+  v = (cand >> lane & 1) ? (unsigned)hi : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+  cand &= __ballot_sync(FULLMASK, v == mn);
+  v = (cand >> lane & 1) ? (unsigned)(lo >> 32) : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+  cand &= __ballot_sync(FULLMASK, v == mn);
+  v = (cand >> lane & 1) ? (unsigned)lo : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
+  cand &= __ballot_sync(FULLMASK, v == mn);
+  return __ffs(cand) - 1;
+}
+
+__device__ __forceinline__ unsigned long long warp_min64(unsigned long long x, int lane) {
+  unsigned v = (unsigned)(x >> 32), mn = __reduce_min_sync(FULLMASK, v);
+  unsigned lo = v == mn ? (unsigned)x : 0xffffffffu;
+  unsigned mlo = __reduce_min_sync(FULLMASK, lo);
+  return ((unsigned long long)mn << 32) | mlo;
+}
+
 __device__ __forceinline__ bool push2(bool want, double ready, unsigned long long key, double exe, int q, int &n,
-                                      const DevProb &P, const W2 &w, int lane) {
+                                      int &nb, unsigned long long &minb, const DevProb &P, const W2 &w, int lane) {
   unsigned bm = __ballot_sync(FULLMASK, want);
   if (!bm) return true;
   int total = __popc(bm);
-  if (n + total > w.rcap) return false;
+  int room = w.rcap - n;
+  if (total > room) {
+    // the front set is full: the rest go to the back set (minb: their lower bound)
+    int spill = total - room;  // (room >= 0: the front set never exceeds its capacity)
+    if (nb + spill > w.bcap) return false;
+    int pos = __popc(bm & ((1u << lane) - 1u));
+    unsigned long long hb = (unsigned long long)__double_as_longlong(ready);
+    if (want) {
+      REnt r;
+      r.h = hb; r.k = key; r.e = exe; r.q = q; r.pad = 0;
+      if (pos < room) w.rs[n + pos] = r;
+      else w.bq[nb + pos - room] = r;
+    }
+    minb = min(minb, warp_min64(want && pos >= room ? hb : ~0ull, lane));
+    n += room;
+    nb += spill;
+    return true;
+  }
   if (want) {
     int pos = n + __popc(bm & ((1u << lane) - 1u));
     REnt r;
@@ -718,26 +792,6 @@ __device__ __forceinline__ int group_of2(const DevProb &P, int op, int g, int k,
   for (int i = 0; i < nd; ++i)
     if (pm >> i & 1) si = si * P.map_deg[g * PS_MAXDIM + i] + coords[i];
   return si;
-}
-
-// warp-wide lexicographic min of 64-bit (hi, lo) pairs; returns winning lane
-__device__ __forceinline__ int warp_argmin128(unsigned long long hi, unsigned long long lo, int lane) {
-  unsigned cand = FULLMASK, v, mn;
-  v = (unsigned)(hi >> 32); mn = __reduce_min_sync(FULLMASK, v); cand = __ballot_sync(FULLMASK, v == mn);
-  v = (cand >> lane & 1) ? (unsigned)hi : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
-  cand &= __ballot_sync(FULLMASK, v == mn);
-  v = (cand >> lane & 1) ? (unsigned)(lo >> 32) : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
-  cand &= __ballot_sync(FULLMASK, v == mn);
-  v = (cand >> lane & 1) ? (unsigned)lo : 0xffffffffu; mn = __reduce_min_sync(FULLMASK, v);
-  cand &= __ballot_sync(FULLMASK, v == mn);
-  return __ffs(cand) - 1;
-}
-
-__device__ __forceinline__ unsigned long long warp_min64(unsigned long long x, int lane) {
-  unsigned v = (unsigned)(x >> 32), mn = __reduce_min_sync(FULLMASK, v);
-  unsigned lo = v == mn ? (unsigned)x : 0xffffffffu;
-  unsigned mlo = __reduce_min_sync(FULLMASK, lo);
-  return ((unsigned long long)mn << 32) | mlo;
 }
 
 // Candidate setup: maps, dense bases, staged overlap offsets, state placement.
@@ -991,6 +1045,157 @@ __device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const 
   copy16(dst + sl.rd, st.ready, 8 * (size_t)nc, lane);
 }
 
+// ---- two-level ready set helpers (warp_simulate2)
+
+// LB over the back set: min over entries with successors of max(ready, clock) + exe
+__device__ __forceinline__ unsigned long long back_lb(const W2 &w, int nb, int lane) {
+  unsigned long long lb = INF_BITS;
+  for (int i = lane; i < nb; i += 32) {
+    REnt e = w.bq[i];
+    if (!(e.q & Q_SINK)) {
+      double r0 = __longlong_as_double((long long)e.h), ck = w.qclock[e.q & Q_MASK];
+      unsigned long long eb = (unsigned long long)__double_as_longlong((r0 < ck ? ck : r0) + e.e);
+      lb = eb < lb ? eb : lb;
+    }
+  }
+  return warp_min64(lb, lane);
+}
+
+// Move every back entry ready before X (bits) to the front set, compacting the
+// back set and recomputing its bound.  If they do not all fit, X drops to the
+// largest of 32 evenly spaced boundaries in [minb, X) below which they do (the
+// moved set stays downward closed: every entry ready before the new X moves);
+// false (nothing moved) if not even the first boundary fits.
+__device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsigned long long &minb,
+                                            unsigned long long X, int lane) {
+  int cnt = 0;
+  for (int i = lane; i < nb; i += 32) cnt += w.bq[i].h < X ? 1 : 0;
+  cnt = (int)__reduce_add_sync(FULLMASK, (unsigned)cnt);
+  const int room = w.rcap - n;
+  if (cnt > room) {
+    if (X == ~0ull || room < 1) return false;
+    // boundary j (lane j): minb + (X - minb) (j + 1) / 32, the last one X itself
+    const double lo = __longlong_as_double((long long)minb), hi = __longlong_as_double((long long)X);
+    // (non-decreasing in the lane: monotone rounding, clamped to X)
+    unsigned long long bj =
+        lane == 31 ? X : (unsigned long long)__double_as_longlong(lo + (hi - lo) * ((double)(lane + 1) * 0.03125));
+    bj = bj < X ? bj : X;
+    int *hist = w.mem;  // (free between rounds: the member list of the slow path)
+    hist[lane] = 0;
+    __syncwarp();
+    for (int base = 0; base < nb; base += 32) {
+      int i = base + lane;
+      unsigned long long h = i < nb ? w.bq[i].h : ~0ull;
+      int b = 0;  // first boundary above h (h < X)
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        unsigned long long x = __shfl_sync(FULLMASK, bj, b + st - 1);
+        if (!(h < x)) b += st;
+      }
+      if (h < X) atomicAdd(&hist[b], 1);
+    }
+    __syncwarp();
+    int c = hist[lane];  // entries ready before boundary `lane`: inclusive scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(FULLMASK, c, off);
+      if (lane >= off) c += y;
+    }
+    unsigned ok = __ballot_sync(FULLMASK, c <= room);  // a leading run (c is non-decreasing)
+    __syncwarp();
+    const int cj = __shfl_sync(FULLMASK, c, max(__popc(ok) - 1, 0));
+    // (at least the back set's earliest entry must move: the front set then
+    // holds the global minimum for a round without members)
+    if (!(ok & 1u) || cj == 0) return false;
+    X = __shfl_sync(FULLMASK, bj, __popc(ok) - 1);
+  }
+  int kept = 0;
+  unsigned long long mb = ~0ull;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = 0; base < nb; base += 32) {
+    int i = base + lane;
+    bool v = i < nb;
+    REnt e;
+    if (v) e = w.bq[i];
+    bool mv = v && e.h < X, kp = v && !mv;
+    unsigned bm = __ballot_sync(FULLMASK, mv), bk = __ballot_sync(FULLMASK, kp);
+    __syncwarp();  // (in-place compaction: every lane has read its entry)
+    if (mv) w.rs[n + __popc(bm & lt)] = e;
+    if (kp) {
+      w.bq[kept + __popc(bk & lt)] = e;
+      mb = e.h < mb ? e.h : mb;
+    }
+    n += __popc(bm);
+    kept += __popc(bk);
+  }
+  nb = kept;
+  minb = warp_min64(mb, lane);
+  __syncwarp();
+  return true;
+}
+
+// Keep about the 32 earliest front entries: T = the 33rd smallest ready time
+// among the first 128 (bitonic sort, four per lane); entries ready at or after
+// T move to the back set, whose bound becomes min(minb, T).  Any T is exact
+// (only the split changes).
+__device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigned long long &minb, int lane) {
+  unsigned long long v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int i = j * 32 + lane;
+    v[j] = i < n ? w.rs[i].h : ~0ull;
+  }
+#pragma unroll
+  for (int k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+    for (int sd = k >> 1; sd > 0; sd >>= 1) {
+      if (sd >= 32) {
+        const int js = sd >> 5;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j & js) continue;
+          const int j2 = j | js;
+          const bool up = ((j * 32 + lane) & k) == 0;
+          unsigned long long a = v[j], b = v[j2];
+          if ((a > b) == up) { v[j] = b; v[j2] = a; }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          unsigned long long o = __shfl_xor_sync(FULLMASK, v[j], sd);
+          const bool up = ((j * 32 + lane) & k) == 0, lower = (lane & sd) == 0;
+          v[j] = (lower == up) ? (v[j] < o ? v[j] : o) : (v[j] > o ? v[j] : o);
+        }
+      }
+    }
+  }
+  const unsigned long long T = __shfl_sync(FULLMASK, v[1], 0), lo = __shfl_sync(FULLMASK, v[0], 0);
+  if (T == lo) return true;  // (ties at the minimum: keep everything)
+  int evict = 0;
+  for (int i = lane; i < n; i += 32) evict += w.rs[i].h >= T ? 1 : 0;
+  evict = (int)__reduce_add_sync(FULLMASK, (unsigned)evict);
+  if (nb + evict > w.bcap) return false;
+  int kept = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = 0; base < n; base += 32) {
+    int i = base + lane;
+    bool v2 = i < n;
+    REnt e;
+    if (v2) e = w.rs[i];
+    bool ev = v2 && e.h >= T, kp = v2 && !ev;
+    unsigned be = __ballot_sync(FULLMASK, ev), bk = __ballot_sync(FULLMASK, kp);
+    __syncwarp();
+    if (ev) w.bq[nb + __popc(be & lt)] = e;
+    if (kp) w.rs[kept + __popc(bk & lt)] = e;
+    nb += __popc(be);
+    kept += __popc(bk);
+  }
+  n = kept;
+  minb = T < minb ? T : minb;
+  __syncwarp();
+  return true;
+}
+
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
@@ -1078,6 +1283,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   }
   __syncwarp();
   int n = 0;
+  int nb = 0;                  // back ready set size
+  unsigned long long minb = ~0ull;  // lower bound of the back set's ready times (bits; ~0: empty)
   bool okc = true;
   int round = 0, next_snap = 0x7fffffff;  // (SNAP) round counter, round of the next snapshot
   if (SNAP && w.dc->restore) {
@@ -1162,7 +1369,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe, SIMPLE);
         want = true;
       }
-      okc &= push2(want, 0.0, key, exe, q, n, P, w, lane);
+      okc &= push2(want, 0.0, key, exe, q, n, nb, minb, P, w, lane);
     }
   }
   if (SNAP) {
@@ -1172,9 +1379,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   __syncwarp();
   PH_ADD(1, t_init);
   if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
-  while (n > 0) {
+  while (n > 0 || nb > 0) {
     if (SNAP && round == next_snap) {
-      snap_write(P, w, st, n, round, round / w.dc->stride, out.makespan, FULL, lane);
+      // (a state with a back set is not snapshotted: the index is marked unusable)
+      snap_write(P, w, st, nb ? P.cap + 1 : n, round, round / w.dc->stride, out.makespan, FULL, lane);
       next_snap = round / w.dc->stride + 1 < w.dc->nsnap ? round + w.dc->stride : 0x7fffffff;
     }
     PH_T(t_sel);
@@ -1193,9 +1401,40 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     // Medium path (33..64 ready tasks, two per lane): when the round's members
     // are at most 32, they are staged at [64, 64 + members) and the others
     // compacted to [0, rest); the fast path below then runs the members alone.
-    int sel_base = 0, sel_n = n, rest = 0;
+    // Two-level ready set.  With a back set, the round's members must also be
+    // ready before every back entry (minb bounds them below), and the front
+    // set alone must determine LB: if the back set could hold a member or an
+    // earlier bound (minb < LB of the front set), its entries ready before that
+    // LB move to the front set first -- or, if they do not fit, this round runs
+    // over both sets in the back set (bslow).
+    bool bslow = false;
+    if (nb > 0) {
+      unsigned long long lbf = INF_BITS;
+      for (int i = lane; i < n; i += 32) {
+        REnt e = w.rs[i];
+        if (!(e.q & Q_SINK)) {
+          double r0 = __longlong_as_double((long long)e.h), ck = w.qclock[e.q & Q_MASK];
+          unsigned long long eb = (unsigned long long)__double_as_longlong((r0 < ck ? ck : r0) + e.e);
+          lbf = eb < lbf ? eb : lbf;
+        }
+      }
+      lbf = warp_min64(lbf, lane);
+      if (n == 0 || minb < lbf) {
+        unsigned long long X = n ? lbf : back_lb(w, nb, lane);
+        if (X == INF_BITS) X = ~0ull;  // no entry with successors: every entry is a member
+        if (!back_refill(w, n, nb, minb, X, lane)) {
+          if (nb + n > w.bcap) { out.status = PS_STATUS_CAPACITY; return out; }
+          for (int i = lane; i < n; i += 32) w.bq[nb + i] = w.rs[i];
+          nb += n;
+          n = 0;
+          bslow = true;
+          __syncwarp();
+        }
+      }
+    }
+    int sel_base = 0, sel_n = bslow ? 33 : n, rest = 0;
     bool forced = false;
-    if (n > 32 && n <= 64 && n + 32 <= w.rcap) {
+    if (!bslow && n > 32 && n <= 64 && n + 32 <= w.rcap) {
       bool vA = true, vB = lane + 32 < n;
       unsigned long long hA = w.rs[lane].h, kA = w.rs[lane].k, hB = vB ? w.rs[lane + 32].h : ~0ull,
                          kB = vB ? w.rs[lane + 32].k : ~0ull;
@@ -1207,7 +1446,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       unsigned long long bA = !(qA & Q_SINK) ? (unsigned long long)__double_as_longlong(lA) : INF_BITS;
       unsigned long long bB = (vB && !(qB & Q_SINK)) ? (unsigned long long)__double_as_longlong(lB) : INF_BITS;
       double LB2 = __longlong_as_double((long long)warp_min64(bA < bB ? bA : bB, lane));
-      bool mA = vA && rA < LB2, mB = vB && rB < LB2;
+      bool mA = vA && rA < LB2 && hA < minb, mB = vB && rB < LB2 && hB < minb;
       unsigned gA = __ballot_sync(FULLMASK, mA), gB = __ballot_sync(FULLMASK, mB);
       int nm = __popc(gA) + __popc(gB);
       if (nm > 0 && nm <= 32) {
@@ -1242,7 +1481,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       PH_ADD(5, t_sel);
       TC(2);
       PH_T(t_cl);
-      bool member = valid && (forced || r < LB);
+      bool member = valid && (forced || (r < LB && h < minb));
       if (!__any_sync(FULLMASK, member)) {
         // degenerate (zero or absorbed exe): the global minimum alone
         int wl = warp_argmin128(h, k, lane);
@@ -1295,20 +1534,26 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       TC(6);
       PH_ADD(15, t_cl);
     } else {
+      // ---- slow path: the front set (more than 64 entries, or more than 32
+      // members), or -- bslow -- front and back sets together in the back set
+      REnt *S = bslow ? w.bq : w.rs;
+      int *SM = bslow ? w.bmem : w.mem;
+      int sn = bslow ? nb : n;
+      const unsigned long long mbk = bslow ? ~0ull : minb;  // members: ready below the back set too
       PH_T(t_slow);
       PH_CNT(16, 1);
-      PH_CNT(17, n);
+      PH_CNT(17, sn);
       if (lane == 0) w.flags[0] = 1;
       dirty = true;
       // ---- scan 1: minimum key and LB = min(ready + exe)
       unsigned long long bh = ~0ull, bl = ~0ull, lb = INF_BITS;
-      for (int i = lane; i < n; i += 32) {
-        unsigned long long h = w.rs[i].h, l = w.rs[i].k;
+      for (int i = lane; i < sn; i += 32) {
+        unsigned long long h = S[i].h, l = S[i].k;
         if (h < bh || (h == bh && l < bl)) { bh = h; bl = l; }
-        int qr = w.rs[i].q;
+        int qr = S[i].q;
         if (!(qr & Q_SINK)) {
           double r0 = __longlong_as_double((long long)h), ck = w.qclock[qr & Q_MASK];
-          double e = (r0 < ck ? ck : r0) + w.rs[i].e;
+          double e = (r0 < ck ? ck : r0) + S[i].e;
           unsigned long long eb = (unsigned long long)__double_as_longlong(e);
           if (eb < lb) lb = eb;
         }
@@ -1319,24 +1564,24 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       // ---- scan 2: members (ready < LB, or the global minimum) -> member list,
       // and each bids its ready time for its queue
       int nm = 0;
-      for (int base = 0; base < n; base += 32) {
+      for (int base = 0; base < sn; base += 32) {
         int i = base + lane;
         bool mem = false;
-        if (i < n) {
-          unsigned long long h2 = w.rs[i].h;
-          mem = __longlong_as_double((long long)h2) < LB || w.rs[i].k == minkey;
-          if (mem) atomicMin(&w.qready[w.rs[i].q & Q_MASK], h2);
+        if (i < sn) {
+          unsigned long long h2 = S[i].h;
+          mem = (__longlong_as_double((long long)h2) < LB && h2 < mbk) || S[i].k == minkey;
+          if (mem) atomicMin(&w.qready[S[i].q & Q_MASK], h2);
         }
         unsigned bm = __ballot_sync(FULLMASK, mem);
-        if (mem) w.mem[nm + __popc(bm & ((1u << lane) - 1u))] = i;
+        if (mem) SM[nm + __popc(bm & ((1u << lane) - 1u))] = i;
         nm += __popc(bm);
       }
       __syncwarp();
       // ---- members tied on their queue's ready time bid their origin key
       for (int j = lane; j < nm; j += 32) {
-        int i = w.mem[j];
-        int q2 = w.rs[i].q & Q_MASK;
-        if (w.qready[q2] == w.rs[i].h) atomicMin(&w.qbest[q2], w.rs[i].k);
+        int i = SM[j];
+        int q2 = S[i].q & Q_MASK;
+        if (w.qready[q2] == S[i].h) atomicMin(&w.qbest[q2], S[i].k);
       }
       __syncwarp();
       // ---- winners: each queue's minimum (ready, origin); lane k holds winner k
@@ -1346,9 +1591,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         bool win = false;
         int i = 0;
         if (j < nm) {
-          i = w.mem[j];
-          int q2 = w.rs[i].q & Q_MASK;
-          win = w.qbest[q2] == w.rs[i].k && w.qready[q2] == w.rs[i].h;
+          i = SM[j];
+          int q2 = S[i].q & Q_MASK;
+          win = w.qbest[q2] == S[i].k && w.qready[q2] == S[i].h;
         }
         unsigned bm = __ballot_sync(FULLMASK, win);
         // lane nw + r takes the r-th winner of this chunk (winners past 32 wait)
@@ -1360,35 +1605,37 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       bool mine0 = lane < nw;
       if (mine0) {
-        mykey = w.rs[mypos].k;
-        myready = __longlong_as_double((long long)w.rs[mypos].h);
-        myexe = w.rs[mypos].e;
-        myq = w.rs[mypos].q & Q_MASK;
+        mykey = S[mypos].k;
+        myready = __longlong_as_double((long long)S[mypos].h);
+        myexe = S[mypos].e;
+        myq = S[mypos].q & Q_MASK;
       }
       __syncwarp();
-      if (mine0) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; w.rs[mypos].h = ~0ull; }
+      if (mine0) { w.qbest[myq] = ~0ull; w.qready[myq] = ~0ull; S[mypos].h = ~0ull; }
       __syncwarp();
-      // ---- remove the winners: refill holes below n-nw with survivors from the tail
+      // ---- remove the winners: refill holes below sn-nw with survivors from the tail
       {
-        int tailpos = n - nw + lane;
-        bool survivor = lane < nw && w.rs[tailpos].h != ~0ull;
+        int tailpos = sn - nw + lane;
+        bool survivor = lane < nw && S[tailpos].h != ~0ull;
         unsigned sm = __ballot_sync(FULLMASK, survivor);
-        bool head_hole = mine0 && mypos < n - nw;
+        bool head_hole = mine0 && mypos < sn - nw;
         unsigned hm = __ballot_sync(FULLMASK, head_hole);
         int hrank = __popc(hm & ((1u << lane) - 1u));
         int src = -1;
-        if (head_hole) src = n - nw + (int)__fns(sm, 0, hrank + 1);
+        if (head_hole) src = sn - nw + (int)__fns(sm, 0, hrank + 1);
         unsigned long long h2 = 0, k2 = 0;
         double e2 = 0.0;
         int q2 = 0;
-        if (head_hole) { h2 = w.rs[src].h; k2 = w.rs[src].k; e2 = w.rs[src].e; q2 = w.rs[src].q; }
+        if (head_hole) { h2 = S[src].h; k2 = S[src].k; e2 = S[src].e; q2 = S[src].q; }
         __syncwarp();
-        if (head_hole) { w.rs[mypos].h = h2; w.rs[mypos].k = k2; w.rs[mypos].e = e2; w.rs[mypos].q = q2; }
-        n -= nw;
+        if (head_hole) { S[mypos].h = h2; S[mypos].k = k2; S[mypos].e = e2; S[mypos].q = q2; }
+        sn -= nw;
         __syncwarp();
       }
       mine = lane < nw;
       w.wlane[lane] = lane;
+      if (bslow) { nb = sn; minb = 0ull; }  // (0: a valid lower bound until the next refill)
+      else n = sn;
       PH_ADD(19, t_slow);
       PH_CNT(18, nw);
     }
@@ -1621,7 +1868,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           return out;
         }
       }
-      if (!push2(want, pready, skey, pexe, pq, n, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+      if (!push2(want, pready, skey, pexe, pq, n, nb, minb, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
       __syncwarp();
     }
     PH_ADD(4, t_it);
@@ -1630,6 +1877,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     ++tc_r;
 #endif
     if (SNAP) ++round;
+    // keep the front set small: past 64 entries, the later ones move to the back set
+    if (n > 64 && w.bcap) {
+      if (!front_trim(w, n, nb, minb, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+    }
     // (no barrier here: every path above ends with one after its last shared store)
   }
   if (SNAP && lane == 0) w.dc->rounds = round;
@@ -2508,10 +2759,13 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
       pr->lay.tab_bytes = 0;
       pr->lay.warp_bytes = al16(warp_bytes_of(P, pr->lay.SC, pr->lay.GC, pr->lay.RC, 1));
       pr->wpb = 8;
-      pr->smem_per_block = 0;
+      pr->lay.hot_bytes = (int)al16(hot_bytes_of(P));
+      if ((size_t)pr->wpb * pr->lay.hot_bytes > (size_t)optin || getenv("PS_NO_HOT")) pr->lay.hot_bytes = 0;
+      pr->smem_per_block = (size_t)pr->wpb * pr->lay.hot_bytes;
       bestW = 8; bestWarps = 8; bestSC = pr->lay.SC;
     } else {
       pr->lay.global_all = 0;
+      pr->lay.hot_bytes = 0;
     pr->lay.tab_bytes = tb;
     pr->lay.SC = bestSC;
     pr->lay.GC = bestGC;
@@ -2684,7 +2938,7 @@ int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   TraceSink tr;
   tr.tasks = dt; tr.task_cap = task_cap; tr.n_tasks = cnts; tr.edge_pred = dep; tr.edge_succ = des;
   tr.edge_cap = edge_cap; tr.n_edges = cnts + 1;
-  size_t smem = pr->lay.global_all ? 0 : pr->lay.tab_bytes + pr->lay.warp_bytes;
+  size_t smem = pr->lay.global_all ? pr->lay.hot_bytes : pr->lay.tab_bytes + pr->lay.warp_bytes;
   k_simulate_trace<<<1, 32, smem>>>(pr->P, pr->lay, pr->d_map, pr->d_asg, scr, tr, dmk, err + 2, err);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
