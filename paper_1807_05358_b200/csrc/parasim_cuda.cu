@@ -685,7 +685,7 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
 // simulator variants: SIM_TRACE records every task and dependency
 // (k_simulate_trace), SIM_OPMIN keeps each op's earliest forward end (exhaustive
 // search bounds); the MCMC kernel compiles neither
-enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4, SIM_FULL = 8, SIM_FWD = 16, SIM_SNAP = 32 };
+enum { SIM_TRACE = 1, SIM_OPMIN = 2, SIM_SIMPLE = 4, SIM_FULL = 8, SIM_FWD = 16, SIM_SNAP = 32, SIM_BACK = 64 };
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane);
 
@@ -747,13 +747,15 @@ __device__ __forceinline__ unsigned long long warp_min64(unsigned long long x, i
   return ((unsigned long long)mn << 32) | mlo;
 }
 
+template <bool BACK>
 __device__ __forceinline__ bool push2(bool want, double ready, unsigned long long key, double exe, int q, int &n,
                                       int &nb, unsigned long long &minb, const DevProb &P, const W2 &w, int lane) {
   unsigned bm = __ballot_sync(FULLMASK, want);
   if (!bm) return true;
   int total = __popc(bm);
   int room = w.rcap - n;
-  if (total > room) {
+  if (!BACK && total > room) return false;  // (the caller re-runs with the ready set in global memory)
+  if (BACK && total > room) {
     // the front set is full: the rest go to the back set (minb: their lower bound)
     int spill = total - room;  // (room >= 0: the front set never exceeds its capacity)
     if (nb + spill > w.bcap) return false;
@@ -1063,51 +1065,70 @@ __device__ __forceinline__ unsigned long long back_lb(const W2 &w, int nb, int l
 
 // Move every back entry ready before X (bits) to the front set, compacting the
 // back set and recomputing its bound.  If they do not all fit, X drops to the
-// largest of 32 evenly spaced boundaries in [minb, X) below which they do (the
-// moved set stays downward closed: every entry ready before the new X moves);
-// false (nothing moved) if not even the first boundary fits.
+// largest of 32 evenly spaced boundaries between the back set's earliest ready
+// time and X below which they do (refined twice more inside the first
+// interval when even it overflows); the moved set stays downward closed, and
+// holds at least the back set's earliest entry.  False (nothing moved) if no
+// such boundary is found.
 __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsigned long long &minb,
                                             unsigned long long X, int lane) {
   int cnt = 0;
-  for (int i = lane; i < nb; i += 32) cnt += w.bq[i].h < X ? 1 : 0;
+  unsigned long long mn = ~0ull;
+  for (int i = lane; i < nb; i += 32) {
+    unsigned long long h = w.bq[i].h;
+    cnt += h < X ? 1 : 0;
+    mn = h < mn ? h : mn;
+  }
   cnt = (int)__reduce_add_sync(FULLMASK, (unsigned)cnt);
   const int room = w.rcap - n;
   if (cnt > room) {
     if (X == ~0ull || room < 1) return false;
-    // boundary j (lane j): minb + (X - minb) (j + 1) / 32, the last one X itself
-    const double lo = __longlong_as_double((long long)minb), hi = __longlong_as_double((long long)X);
-    // (non-decreasing in the lane: monotone rounding, clamped to X)
-    unsigned long long bj =
-        lane == 31 ? X : (unsigned long long)__double_as_longlong(lo + (hi - lo) * ((double)(lane + 1) * 0.03125));
-    bj = bj < X ? bj : X;
-    int *hist = w.mem;  // (free between rounds: the member list of the slow path)
-    hist[lane] = 0;
-    __syncwarp();
-    for (int base = 0; base < nb; base += 32) {
-      int i = base + lane;
-      unsigned long long h = i < nb ? w.bq[i].h : ~0ull;
-      int b = 0;  // first boundary above h (h < X)
+    mn = warp_min64(mn, lane);
+    int *hist = w.wlane;  // (32 ints, free until the round picks its winners)
+    unsigned long long hiX = X;
+    bool found = false;
+#pragma unroll 1
+    for (int level = 0; level < 3 && !found; ++level) {
+      // boundary j (lane j): mn + (hiX - mn) (j + 1) / 32, the last one hiX itself
+      // (non-decreasing in the lane: monotone rounding, clamped to hiX)
+      const double lo = __longlong_as_double((long long)mn), hi = __longlong_as_double((long long)hiX);
+      unsigned long long bj = lane == 31 ? hiX
+                                         : (unsigned long long)__double_as_longlong(
+                                               lo + (hi - lo) * ((double)(lane + 1) * 0.03125));
+      bj = bj < hiX ? bj : hiX;
+      hist[lane] = 0;
+      __syncwarp();
+      for (int base = 0; base < nb; base += 32) {
+        int i = base + lane;
+        unsigned long long h = i < nb ? w.bq[i].h : ~0ull;
+        int b = 0;  // first boundary above h (when h < hiX)
 #pragma unroll
-      for (int st = 16; st >= 1; st >>= 1) {
-        unsigned long long x = __shfl_sync(FULLMASK, bj, b + st - 1);
-        if (!(h < x)) b += st;
+        for (int st = 16; st >= 1; st >>= 1) {
+          unsigned long long x = __shfl_sync(FULLMASK, bj, b + st - 1);
+          if (!(h < x)) b += st;
+        }
+        if (h < hiX) atomicAdd(&hist[b], 1);
       }
-      if (h < X) atomicAdd(&hist[b], 1);
-    }
-    __syncwarp();
-    int c = hist[lane];  // entries ready before boundary `lane`: inclusive scan
+      __syncwarp();
+      int c = hist[lane];  // entries ready before boundary `lane`: inclusive scan
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      int y = __shfl_up_sync(FULLMASK, c, off);
-      if (lane >= off) c += y;
+      for (int off = 1; off < 32; off <<= 1) {
+        int y = __shfl_up_sync(FULLMASK, c, off);
+        if (lane >= off) c += y;
+      }
+      unsigned ok = __ballot_sync(FULLMASK, c <= room);  // a leading run (c is non-decreasing)
+      __syncwarp();
+      const int jb = __popc(ok) - 1;
+      const int cj = __shfl_sync(FULLMASK, c, max(jb, 0));
+      if (jb >= 0 && cj > 0) {
+        X = __shfl_sync(FULLMASK, bj, jb);
+        found = true;
+      } else {
+        hiX = __shfl_sync(FULLMASK, bj, 0);  // refine inside the first interval
+        if (hiX <= mn) break;
+      }
     }
-    unsigned ok = __ballot_sync(FULLMASK, c <= room);  // a leading run (c is non-decreasing)
-    __syncwarp();
-    const int cj = __shfl_sync(FULLMASK, c, max(__popc(ok) - 1, 0));
-    // (at least the back set's earliest entry must move: the front set then
-    // holds the global minimum for a round without members)
-    if (!(ok & 1u) || cj == 0) return false;
-    X = __shfl_sync(FULLMASK, bj, __popc(ok) - 1);
+    if (!found) return false;
   }
   int kept = 0;
   unsigned long long mb = ~0ull;
@@ -1200,6 +1221,7 @@ template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
   constexpr bool SNAP = (M & SIM_SNAP) != 0;      // delta evaluation: snapshots, first rounds, resume
+  constexpr bool BACK = (M & SIM_BACK) != 0;      // wide problems: two-level ready set (front + back)
   // mode known at compile time in the specialised variants (forward mode then
   // drops every backward / ring path)
   constexpr int MODE = (M & SIM_FULL) ? 1 : (M & SIM_FWD) ? 0 : -1;
@@ -1369,7 +1391,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         op_attrs(P, T, w, KIND_OP, o, s - w.fbase[o], q, exe, SIMPLE);
         want = true;
       }
-      okc &= push2(want, 0.0, key, exe, q, n, nb, minb, P, w, lane);
+      okc &= push2<BACK>(want, 0.0, key, exe, q, n, nb, minb, P, w, lane);
     }
   }
   if (SNAP) {
@@ -1379,7 +1401,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   __syncwarp();
   PH_ADD(1, t_init);
   if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
-  while (n > 0 || nb > 0) {
+  while (n > 0 || (BACK && nb > 0)) {
     if (SNAP && round == next_snap) {
       // (a state with a back set is not snapshotted: the index is marked unusable)
       snap_write(P, w, st, nb ? P.cap + 1 : n, round, round / w.dc->stride, out.makespan, FULL, lane);
@@ -1408,7 +1430,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     // LB move to the front set first -- or, if they do not fit, this round runs
     // over both sets in the back set (bslow).
     bool bslow = false;
-    if (nb > 0) {
+    if (BACK && nb > 0) {
       unsigned long long lbf = INF_BITS;
       for (int i = lane; i < n; i += 32) {
         REnt e = w.rs[i];
@@ -1446,7 +1468,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       unsigned long long bA = !(qA & Q_SINK) ? (unsigned long long)__double_as_longlong(lA) : INF_BITS;
       unsigned long long bB = (vB && !(qB & Q_SINK)) ? (unsigned long long)__double_as_longlong(lB) : INF_BITS;
       double LB2 = __longlong_as_double((long long)warp_min64(bA < bB ? bA : bB, lane));
-      bool mA = vA && rA < LB2 && hA < minb, mB = vB && rB < LB2 && hB < minb;
+      bool mA = vA && rA < LB2 && (!BACK || hA < minb), mB = vB && rB < LB2 && (!BACK || hB < minb);
       unsigned gA = __ballot_sync(FULLMASK, mA), gB = __ballot_sync(FULLMASK, mB);
       int nm = __popc(gA) + __popc(gB);
       if (nm > 0 && nm <= 32) {
@@ -1481,7 +1503,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       PH_ADD(5, t_sel);
       TC(2);
       PH_T(t_cl);
-      bool member = valid && (forced || (r < LB && h < minb));
+      bool member = valid && (forced || (r < LB && (!BACK || h < minb)));
       if (!__any_sync(FULLMASK, member)) {
         // degenerate (zero or absorbed exe): the global minimum alone
         int wl = warp_argmin128(h, k, lane);
@@ -1539,7 +1561,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       REnt *S = bslow ? w.bq : w.rs;
       int *SM = bslow ? w.bmem : w.mem;
       int sn = bslow ? nb : n;
-      const unsigned long long mbk = bslow ? ~0ull : minb;  // members: ready below the back set too
+      const unsigned long long mbk = (!BACK || bslow) ? ~0ull : minb;  // members: ready below the back set too
       PH_T(t_slow);
       PH_CNT(16, 1);
       PH_CNT(17, sn);
@@ -1560,6 +1582,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       int wl = warp_argmin128(bh, bl, lane);
       unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
+      const unsigned long long minready = __shfl_sync(FULLMASK, bh, wl);
       double LB = __longlong_as_double((long long)warp_min64(lb, lane));
       // ---- scan 2: members (ready < LB, or the global minimum) -> member list,
       // and each bids its ready time for its queue
@@ -1634,7 +1657,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       mine = lane < nw;
       w.wlane[lane] = lane;
-      if (bslow) { nb = sn; minb = 0ull; }  // (0: a valid lower bound until the next refill)
+      if (bslow) { nb = sn; minb = minready; }  // (the earliest ready time before the round: a lower bound)
       else n = sn;
       PH_ADD(19, t_slow);
       PH_CNT(18, nw);
@@ -1868,7 +1891,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
           return out;
         }
       }
-      if (!push2(want, pready, skey, pexe, pq, n, nb, minb, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+      if (!push2<BACK>(want, pready, skey, pexe, pq, n, nb, minb, P, w, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
       __syncwarp();
     }
     PH_ADD(4, t_it);
@@ -1878,7 +1901,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 #endif
     if (SNAP) ++round;
     // keep the front set small: past 64 entries, the later ones move to the back set
-    if (n > 64 && w.bcap) {
+    if (BACK && n > 64 && w.bcap) {
       if (!front_trim(w, n, nb, minb, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
     }
     // (no barrier here: every path above ends with one after its last shared store)
@@ -2457,6 +2480,29 @@ int upload(std::vector<void *> &owned, const T *host, size_t n, const T **dev) {
 
 }  // namespace
 
+// kernel variant pickers: v = 0 generic, 1 simple full-iteration, 2 simple forward
+typedef void (*BatchKernel)(DevProb, Lay, const int *, const unsigned char *, int, double *, int *, char *, double *,
+                            int *);
+static BatchKernel batch_kernel(int v, bool wide) {
+  if (wide)
+    return v == 0 ? k_simulate_batch<SIM_BACK> : v == 1 ? k_simulate_batch<SIM_BACK | SIM_SIMPLE | SIM_FULL>
+                                                        : k_simulate_batch<SIM_BACK | SIM_SIMPLE | SIM_FWD>;
+  return v == 0 ? k_simulate_batch<0> : v == 1 ? k_simulate_batch<SIM_SIMPLE | SIM_FULL>
+                                               : k_simulate_batch<SIM_SIMPLE | SIM_FWD>;
+}
+typedef void (*McmcKernel)(DevProb, Lay, int, int, int, int, double, double, int *, unsigned char *, int *,
+                           unsigned char *, ChainState *, unsigned *, double *, unsigned char *, int, char *,
+                           unsigned long long, DeltaBufs, Given);
+static McmcKernel mcmc_kernel(int v, bool snap, bool wide) {
+  constexpr int B = SIM_BACK, S = SIM_SNAP, F = SIM_SIMPLE | SIM_FULL, W = SIM_SIMPLE | SIM_FWD;
+  if (wide) {
+    if (snap) return v == 0 ? k_mcmc<B | S> : v == 1 ? k_mcmc<B | S | F> : k_mcmc<B | S | W>;
+    return v == 0 ? k_mcmc<B> : v == 1 ? k_mcmc<B | F> : k_mcmc<B | W>;
+  }
+  if (snap) return v == 0 ? k_mcmc<S> : v == 1 ? k_mcmc<S | F> : k_mcmc<S | W>;
+  return v == 0 ? k_mcmc<0> : v == 1 ? k_mcmc<F> : k_mcmc<W>;
+}
+
 struct ps_problem {
   int device;
   DevProb P;
@@ -2473,6 +2519,7 @@ struct ps_problem {
   int *d_st = nullptr;
   int *d_next = nullptr;  // batch work queue: next candidate to take
   bool simple = false;    // kernels' SIM_SIMPLE variant applies (one kind, <= 2 link classes, full mesh)
+  bool wide = false;      // SIM_BACK variants: two-level ready set (many task slots, or PS_FORCE_WIDE)
   char *mcmc_scratch = nullptr;  // chain scratch kept from the last destroyed MCMC handle
   size_t mcmc_scratch_bytes = 0;
   // chain buffers kept from the last destroyed MCMC handle (create/run/destroy
@@ -2625,6 +2672,7 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
       for (int j = 0; j < P.n_dev; ++j)
         if (i != j && d->link_of[i * P.n_dev + j] < 0) { mesh = false; break; }
     pr->simple = mesh && P.n_cls > 0 && P.n_kinds == 1;
+    pr->wide = P.n_slots >= 4096 || getenv("PS_FORCE_WIDE") != nullptr;
     std::vector<short> l16((size_t)P.n_dev * P.n_dev);
     for (size_t i = 0; i < l16.size(); ++i) {
       int li = d->link_of[i];
@@ -2779,15 +2827,12 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
   }
   // the attribute is per kernel, not per problem: allow the device maximum so
   // problems with different layouts can coexist
-  CK(cudaFuncSetAttribute(k_simulate_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_simulate_batch<SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_simulate_batch<SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<SIM_SNAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  for (int wide = 0; wide < 2; ++wide)
+    for (int v = 0; v < 3; ++v) {
+      CK(cudaFuncSetAttribute(batch_kernel(v, wide), cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      for (int snap = 0; snap < 2; ++snap)
+        CK(cudaFuncSetAttribute(mcmc_kernel(v, snap, wide), cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    }
   CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch<0>, pr->wpb * 32, pr->smem_per_block));
@@ -2893,8 +2938,7 @@ int ps_simulate_batch_ex(ps_problem *pr, const int32_t *map_local, const uint8_t
   }
   if (!pr->d_next) CK(cudaMalloc(&pr->d_next, sizeof(int)));
   CK(cudaMemsetAsync(pr->d_next, 0, sizeof(int), s));
-  auto kb = !pr->simple ? k_simulate_batch<0>
-            : pr->P.full ? k_simulate_batch<SIM_SIMPLE | SIM_FULL> : k_simulate_batch<SIM_SIMPLE | SIM_FWD>;
+  auto kb = batch_kernel(!pr->simple ? 0 : pr->P.full ? 1 : 2, pr->wide);
   kb<<<blocks, wpb * 32, pr->smem_per_block, s>>>(pr->P, pr->lay, dm, da, n, dk, ds, pr->scratch, dop,
                                                                  pr->d_next);
   CK(cudaGetLastError());
@@ -3110,10 +3154,7 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   int wpb = pr->wpb;
   int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
-  auto km = m->db.cd ? (!pr->simple ? k_mcmc<SIM_SNAP>
-                                     : pr->P.full ? k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FULL>
-                                                  : k_mcmc<SIM_SNAP | SIM_SIMPLE | SIM_FWD>)
-                    : (!pr->simple ? k_mcmc<0> : pr->P.full ? k_mcmc<SIM_SIMPLE | SIM_FULL> : k_mcmc<SIM_SIMPLE | SIM_FWD>);
+  auto km = mcmc_kernel(!pr->simple ? 0 : pr->P.full ? 1 : 2, m->db.cd != nullptr, pr->wide);
   km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,

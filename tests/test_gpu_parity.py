@@ -677,3 +677,38 @@ def test_sharded_evaluation_equals_one_launch():
     a = ps.evaluate_strategies(g, topo, prof, strategies, mode=ps.MODE_FULL, max_degree=md)
     b = ps.evaluate_strategies(g, topo, prof, strategies, mode=ps.MODE_FULL, max_degree=md, devices=[0, 0, 0])
     assert list(a) == list(b)
+
+
+@pytest.mark.parametrize("cap", [2, 8, 128])
+def test_two_level_ready_set_matches_oracle(oracle, monkeypatch, cap):
+    """The wide-problem variants (front ready set in shared memory, unsorted
+    back set in global memory with a lower bound on its ready times, refill /
+    trim / combined slow rounds) forced onto small problems with tiny front
+    capacities: batch makespans, traced timelines and MCMC trajectories equal
+    the oracle's."""
+    from paper_1807_05358_b200.lowering import lower
+    from paper_1807_05358_b200.search import _eval_encoded
+    monkeypatch.setenv("PS_FORCE_WIDE", "1")
+    rng = random.Random(cap)
+    cases = [(ps.nmt_like(steps=8, layers=2, batch=64, hidden=64, vocab=64), ps.multi_node_topology(4, 4), 8),
+             (ps.random_dag(300, seed=cap), ps.multi_node_topology(4, 4), 4),
+             (ps.inception_v3(), ps.multi_node_topology(4, 4), 4)]
+    for g, topo, md in cases:
+        prof = ps.CostProfile()
+        strategies = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, md, [rng.randrange(10**6) for _ in range(7)])
+        for mode in (ps.MODE_FORWARD, ps.MODE_FULL):
+            low = lower(g, topo, prof, mode, max_degree=md, strategies=strategies, ready_capacity=cap)
+            maps = np.zeros((len(strategies), low.n_ops), dtype=np.int32)
+            asg = np.zeros((len(strategies), low.n_slots), dtype=np.uint8)
+            for i, s in enumerate(strategies):
+                low.encode(s, maps[i], asg[i])
+            got = _eval_encoded(low, maps, asg, strategies)
+            assert list(got) == list(oracle.makespans(g, topo, prof, mode, strategies)), (g, mode)
+            C = 16
+            init = (strategies * 2)[:C]
+            seeds = [5 + 1000003 * c for c in range(C)]
+            a, _, _, at = _run_mcmc_raw(low, init, seeds, 30, 1, record=30)
+            ref = oracle.mcmc(g, topo, prof, mode, init, seeds, 30, md, rng_mode="philox", threads=8)
+            assert [(s.initial_cost, s.best_cost, s.proposals, s.accepted) for s in a] == \
+                [tuple(r[:4]) for r in ref["summary"]], (mode, cap)
+            assert np.array_equal(at, ref["cand"])
