@@ -339,7 +339,7 @@ EXTRA = {  # name: (chains, step budget ms, distinct starts or None, trace sampl
     "resnet": (1024, 100.0, None, 8),
     "nmt": (4096, 300.0, 64, 4),
     "random1k": (4096, 300.0, 64, 4),
-    "random10k": (4096, 1000.0, 16, 2),
+    "random10k": (4096, 2500.0, 16, 2),
 }
 
 

@@ -354,7 +354,8 @@ struct Lay {  // sizes shared by host and device
   int RC;  // staged row / column offset capacity
   int asg_global;  // device assignment read in place from global memory (very wide problems)
   int global_all;  // block tables and warp slices in global memory (problems too big for shared memory)
-  int hot_bytes;   // global_all: per-warp shared-memory slice for the per-round state (0: none)
+  int hot_bytes;   // warp slice in global memory: per-warp shared-memory slice for the per-round state (0: none)
+  int warp_global; // warp slices in global memory, block tables in shared memory (wide problems)
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -447,6 +448,7 @@ struct DeltaCtx {
   int last;                // out: last snapshot index written
   unsigned bad;            // out: indices whose state did not fit a snapshot
   int rounds;              // out: round count at the end (resumed rounds included)
+  int rounds_fwd;          // out: 1 + the last round in which a forward operator task ran
   int r0;                  // round of the resumed snapshot
   const int *fsrc, *bsrc;  // first rounds of the strategy resumed from (kept below r0)
   ChainDelta ch;           // k_mcmc: the chain's bookkeeping while the kernel runs
@@ -620,7 +622,7 @@ __host__ __device__ inline size_t gscratch_bytes(int n_slots, int n_queues) {
 
 // one warp's global slice: scratch, plus its whole shared-memory layout in global mode
 __host__ __device__ inline size_t gslice_bytes(const DevProb &P, const Lay &L) {
-  return al16(gscratch_bytes(P.n_slots, P.n_queues)) + (L.global_all ? L.warp_bytes : 0);
+  return al16(gscratch_bytes(P.n_slots, P.n_queues)) + ((L.global_all || L.warp_global) ? L.warp_bytes : 0);
 }
 
 // The per-round state -- front ready set, member list, queue clocks, flags and
@@ -647,6 +649,11 @@ __device__ inline void kernel_layout(const DevProb &P, const Lay &L, char *smem,
     tab_from_global(P, T);
     carve_warp(gslice + al16(gscratch_bytes(P.n_slots, P.n_queues)), P, L, w);
     if (L.hot_bytes) carve_hot(smem + (size_t)wib * L.hot_bytes, P, w);
+  } else if (L.warp_global) {
+    carve_tab(smem, P, T);
+    load_tab(P, T);
+    carve_warp(gslice + al16(gscratch_bytes(P.n_slots, P.n_queues)), P, L, w);
+    carve_hot(smem + L.tab_bytes + (size_t)wib * L.hot_bytes, P, w);
   } else {
     carve_tab(smem, P, T);
     load_tab(P, T);
@@ -1074,6 +1081,7 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
                                             unsigned long long X, int lane) {
   int cnt = 0;
   unsigned long long mn = ~0ull;
+#pragma unroll 4
   for (int i = lane; i < nb; i += 32) {
     unsigned long long h = w.bq[i].h;
     cnt += h < X ? 1 : 0;
@@ -1217,6 +1225,16 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
   return true;
 }
 
+// (warp_simulate2) the front set's LB (bits) is known: refill from the back set
+// and restart the round when the back set could matter
+#define BACK_CHECK(LBBITS)                                                                   \
+  if (BACK && nb > 0 && !refilled && minb < (LBBITS)) {                                      \
+    const unsigned long long X_ = (LBBITS) == INF_BITS ? ~0ull : (LBBITS);                   \
+    if (!back_refill(w, n, nb, minb, X_, lane)) pend_bslow = true;                           \
+    refilled = true;                                                                         \
+    continue;                                                                                \
+  }
+
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
   constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
@@ -1306,6 +1324,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   __syncwarp();
   int n = 0;
   int nb = 0;                  // back ready set size
+  bool refilled = false, pend_bslow = false;  // this round refilled / restarts as a combined slow round
+  int last_fwd = 0;            // (SNAP) last round in which a forward operator task ran
   unsigned long long minb = ~0ull;  // lower bound of the back set's ready times (bits; ~0: empty)
   bool okc = true;
   int round = 0, next_snap = 0x7fffffff;  // (SNAP) round counter, round of the next snapshot
@@ -1425,34 +1445,30 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     // compacted to [0, rest); the fast path below then runs the members alone.
     // Two-level ready set.  With a back set, the round's members must also be
     // ready before every back entry (minb bounds them below), and the front
-    // set alone must determine LB: if the back set could hold a member or an
-    // earlier bound (minb < LB of the front set), its entries ready before that
-    // LB move to the front set first -- or, if they do not fit, this round runs
-    // over both sets in the back set (bslow).
+    // set alone must determine LB.  Each selection path below computes the
+    // front set's LB; if the back set could hold a member or an earlier bound
+    // (minb < that LB) its entries ready before that LB move to the front set
+    // and the round restarts (at most one refill per round) -- or, if they do
+    // not fit, the round restarts over both sets in the back set (bslow).  An
+    // empty front set refills against the back set's own LB here.
     bool bslow = false;
-    if (BACK && nb > 0) {
-      unsigned long long lbf = INF_BITS;
-      for (int i = lane; i < n; i += 32) {
-        REnt e = w.rs[i];
-        if (!(e.q & Q_SINK)) {
-          double r0 = __longlong_as_double((long long)e.h), ck = w.qclock[e.q & Q_MASK];
-          unsigned long long eb = (unsigned long long)__double_as_longlong((r0 < ck ? ck : r0) + e.e);
-          lbf = eb < lbf ? eb : lbf;
-        }
-      }
-      lbf = warp_min64(lbf, lane);
-      if (n == 0 || minb < lbf) {
-        unsigned long long X = n ? lbf : back_lb(w, nb, lane);
+    if (BACK && nb > 0 && (n == 0 || pend_bslow)) {
+      bool moved = false;
+      if (!pend_bslow) {
+        unsigned long long X = back_lb(w, nb, lane);
         if (X == INF_BITS) X = ~0ull;  // no entry with successors: every entry is a member
-        if (!back_refill(w, n, nb, minb, X, lane)) {
-          if (nb + n > w.bcap) { out.status = PS_STATUS_CAPACITY; return out; }
-          for (int i = lane; i < n; i += 32) w.bq[nb + i] = w.rs[i];
-          nb += n;
-          n = 0;
-          bslow = true;
-          __syncwarp();
-        }
+        moved = back_refill(w, n, nb, minb, X, lane);
+        refilled = true;
       }
+      if (!moved) {
+        if (nb + n > w.bcap) { out.status = PS_STATUS_CAPACITY; return out; }
+        for (int i = lane; i < n; i += 32) w.bq[nb + i] = w.rs[i];
+        nb += n;
+        n = 0;
+        bslow = true;
+        __syncwarp();
+      }
+      pend_bslow = false;
     }
     int sel_base = 0, sel_n = bslow ? 33 : n, rest = 0;
     bool forced = false;
@@ -1467,7 +1483,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       double lA = (rA < cA ? cA : rA) + eA, lB = (rB < cB ? cB : rB) + eB;
       unsigned long long bA = !(qA & Q_SINK) ? (unsigned long long)__double_as_longlong(lA) : INF_BITS;
       unsigned long long bB = (vB && !(qB & Q_SINK)) ? (unsigned long long)__double_as_longlong(lB) : INF_BITS;
-      double LB2 = __longlong_as_double((long long)warp_min64(bA < bB ? bA : bB, lane));
+      const unsigned long long lb2b = warp_min64(bA < bB ? bA : bB, lane);
+      BACK_CHECK(lb2b);
+      double LB2 = __longlong_as_double((long long)lb2b);
       bool mA = vA && rA < LB2 && (!BACK || hA < minb), mB = vB && rB < LB2 && (!BACK || hB < minb);
       unsigned gA = __ballot_sync(FULLMASK, mA), gB = __ballot_sync(FULLMASK, mB);
       int nm = __popc(gA) + __popc(gB);
@@ -1499,7 +1517,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       double el = (r < ck ? ck : r) + e;
       TC(1);
       unsigned long long lbb = (valid && !(qr & Q_SINK)) ? (unsigned long long)__double_as_longlong(el) : INF_BITS;
-      double LB = __longlong_as_double((long long)warp_min64(lbb, lane));
+      const unsigned long long lbw = warp_min64(lbb, lane);
+      if (!forced) BACK_CHECK(lbw);
+      double LB = __longlong_as_double((long long)lbw);
       PH_ADD(5, t_sel);
       TC(2);
       PH_T(t_cl);
@@ -1583,7 +1603,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       int wl = warp_argmin128(bh, bl, lane);
       unsigned long long minkey = __shfl_sync(FULLMASK, bl, wl);
       const unsigned long long minready = __shfl_sync(FULLMASK, bh, wl);
-      double LB = __longlong_as_double((long long)warp_min64(lb, lane));
+      const unsigned long long lbs = warp_min64(lb, lane);
+      if (!bslow) BACK_CHECK(lbs);
+      double LB = __longlong_as_double((long long)lbs);
       // ---- scan 2: members (ready < LB, or the global minimum) -> member list,
       // and each bids its ready time for its queue
       int nm = 0;
@@ -1674,6 +1696,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         w.qclock[myq] = end;
       }
     }
+    // (full-iteration snapshots only need to cover the forward part: every
+    // resume point lies before the changed op's first forward task)
+    if (SNAP && __any_sync(FULLMASK, mine && key_kind(mykey) == KIND_OP)) last_fwd = round;
     if (mine) {
       if (end > out.makespan) out.makespan = end;
       if ((M & SIM_OPMIN) && key_kind(mykey) == KIND_OP)
@@ -1900,13 +1925,14 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     ++tc_r;
 #endif
     if (SNAP) ++round;
+    refilled = false;
     // keep the front set small: past 64 entries, the later ones move to the back set
     if (BACK && n > 64 && w.bcap) {
       if (!front_trim(w, n, nb, minb, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
     }
     // (no barrier here: every path above ends with one after its last shared store)
   }
-  if (SNAP && lane == 0) w.dc->rounds = round;
+  if (SNAP && lane == 0) { w.dc->rounds = round; w.dc->rounds_fwd = last_fwd + 1; }
   // makespan: max over lanes
   unsigned long long mb = (unsigned long long)__double_as_longlong(out.makespan);
   unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
@@ -2356,7 +2382,10 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
           if (lane == 0) {
             ChainDelta &ch = w.dc->ch;
             if (it < 0 && pass == 0) {
-              int r = w.dc->rounds;
+              // snapshots spread over the rounds that can be resumed from: the
+              // forward part in full-iteration mode (see delta_prepare), all in forward mode
+              const bool fullm = (S & SIM_FULL) ? true : (S & SIM_FWD) ? false : P.full != 0;
+              int r = fullm ? w.dc->rounds_fwd : w.dc->rounds;
               ch.stride = max(4, (r + db.nsnap - 1) / db.nsnap);
             } else {
               ch.rounds_reused += w.dc->r0;
@@ -2800,6 +2829,7 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     if (bestSC < 0) {
       // nothing fits on chip: block tables and warp slices move to global memory
       pr->lay.global_all = 1;
+      pr->lay.warp_global = 0;
       pr->lay.asg_global = 1;
       pr->lay.SC = 3 * P.n_slots + 64;
       pr->lay.GC = P.n_slots + 16;
@@ -2814,6 +2844,7 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     } else {
       pr->lay.global_all = 0;
       pr->lay.hot_bytes = 0;
+      pr->lay.warp_global = 0;
     pr->lay.tab_bytes = tb;
     pr->lay.SC = bestSC;
     pr->lay.GC = bestGC;
@@ -2822,6 +2853,33 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     pr->lay.warp_bytes = al16(warp_bytes_of(P, bestSC, bestGC, bestRC, bestAG));
     pr->wpb = bestW;
     pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
+    // Wide problems whose warp slices keep few warps resident: the slices move
+    // to global memory and only the per-round state stays on chip, when that at
+    // least doubles the resident warps (8 at most: 254 registers per thread)
+    const bool force_wg = getenv("PS_FORCE_WARP_GLOBAL") != nullptr;  // test hook
+    if (pr->wide && (bestWarps < target || force_wg) && !getenv("PS_NO_WARP_GLOBAL")) {
+      size_t hot = al16(hot_bytes_of(P));
+      int cw = 0, cwp = 0;
+      for (int wp : {8, 4, 2}) {
+        size_t blk = tb + wp * hot;
+        if (blk > (size_t)optin) continue;
+        int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
+        int warps = std::min(8, blocks * wp);
+        if (warps > cw) { cw = warps; cwp = wp; }
+      }
+      if (cw >= 2 * bestWarps || (force_wg && cw > 0)) {
+        pr->lay.warp_global = 1;
+        pr->lay.asg_global = 1;
+        pr->lay.SC = 3 * P.n_slots + 64;
+        pr->lay.GC = P.n_slots + 16;
+        pr->lay.RC = 0;
+        pr->lay.hot_bytes = (int)hot;
+        pr->lay.warp_bytes = al16(warp_bytes_of(P, pr->lay.SC, pr->lay.GC, pr->lay.RC, 1));
+        pr->wpb = cwp;
+        pr->smem_per_block = tb + (size_t)cwp * hot;
+        bestW = cwp; bestWarps = cw; bestSC = pr->lay.SC;
+      }
+    }
     }
     pr->blocks_per_sm = std::max(1, bestWarps / bestW);
   }
@@ -2982,7 +3040,9 @@ int ps_simulate_trace(ps_problem *pr, const int32_t *map_local, const uint8_t *a
   TraceSink tr;
   tr.tasks = dt; tr.task_cap = task_cap; tr.n_tasks = cnts; tr.edge_pred = dep; tr.edge_succ = des;
   tr.edge_cap = edge_cap; tr.n_edges = cnts + 1;
-  size_t smem = pr->lay.global_all ? pr->lay.hot_bytes : pr->lay.tab_bytes + pr->lay.warp_bytes;
+  size_t smem = pr->lay.global_all    ? pr->lay.hot_bytes
+                : pr->lay.warp_global ? pr->lay.tab_bytes + pr->lay.hot_bytes
+                                      : pr->lay.tab_bytes + pr->lay.warp_bytes;
   k_simulate_trace<<<1, 32, smem>>>(pr->P, pr->lay, pr->d_map, pr->d_asg, scr, tr, dmk, err + 2, err);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
