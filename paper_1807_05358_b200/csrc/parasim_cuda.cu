@@ -3183,7 +3183,9 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     size_t budget = std::min((size_t)8 << 30, total_b / 16);
-    int ns = (int)std::min<size_t>(24, budget / ((size_t)n * 2 * sb));
+    size_t want_ns = 24;
+    if (const char *e = getenv("PS_NSNAP")) want_ns = (size_t)std::max(4, std::min(31, atoi(e)));
+    int ns = (int)std::min<size_t>(want_ns, budget / ((size_t)n * 2 * sb));
     bool on = params->delta != 0 && P.min_exe > 0.0 && ns >= 4 && !getenv("PS_NO_DELTA");
     if (on) {
       m->db.nsnap = ns;
