@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--budget-ms", type=float, default=100.0,
                     help="time-boxed steps: each chain proposes until this much device time has passed")
     ap.add_argument("--mode", default="full-iteration", choices=("forward", "full-iteration"))
-    ap.add_argument("--config", default="inception", choices=("inception", "alexnet", "resnet", "nmt", "random"))
+    ap.add_argument("--config", default="inception", choices=("inception", "alexnet", "resnet", "nmt", "random", "random1k", "random10k"))
     ap.add_argument("--ops", type=int, default=1000, help="operator count of the random-DAG config")
     ap.add_argument("--no-delta", action="store_true",
                     help="score every proposal from time zero instead of resuming from a snapshot")
