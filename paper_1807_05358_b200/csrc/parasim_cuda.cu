@@ -41,6 +41,10 @@
 #include "parasim.h"
 
 #define FULLMASK 0xffffffffu
+// threads per block the warp kernels are compiled for (registers: 65536 / this)
+#ifndef PS_MAX_THREADS
+#define PS_MAX_THREADS 256
+#endif
 
 namespace {
 
@@ -1942,7 +1946,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 }
 
 template <int S>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(PS_MAX_THREADS, 1)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
                  double *makespan, int *status, char *gscratch, double *opmin, int *next) {
   extern __shared__ __align__(16) char smem[];
@@ -2262,7 +2266,7 @@ struct Given {
 };
 
 template <int S>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(PS_MAX_THREADS, 1)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
@@ -2639,6 +2643,7 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
   P.n_pairs = d->n_pairs; P.n_maps = d->n_maps; P.full = d->mode_full; P.n_slots = d->n_slots;
   P.n_queues = d->n_devices + d->n_links;
   P.cap = d->ready_capacity > 0 ? d->ready_capacity : 128;
+  if (const char *e = getenv("PS_READY_CAP")) P.cap = std::max(2, atoi(e));  // (experiments)
   P.mult = d->backward_multiplier;
   pr->h_map_off.assign(d->op_map_off, d->op_map_off + P.n_ops + 1);
   pr->h_map_size.assign(d->map_size, d->map_size + P.n_maps);
@@ -2803,20 +2808,32 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     for (int c = 4096; c >= 128; c -= 32) caps.push_back(c);
     caps.push_back(0);
     int ag0 = getenv("PS_FORCE_ASG_GLOBAL") ? 1 : 0;  // test hook: exercise the in-place path
+    int rc_frac = 11;  // staged row / column offsets per 16 counters (0: read in place)
+    if (const char *e = getenv("PS_RC_FRAC")) rc_frac = std::max(0, atoi(e));
+    // resident warps per SM the evaluation kernels' registers allow
+    int reg_warps = 64;
+    {
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, mcmc_kernel(1, true, false)) == cudaSuccess && fa.numRegs > 0) {
+        int per_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+        reg_warps = 65536 / per_warp;
+      }
+    }
     for (int ag = ag0; ag < 2 && bestWarps < target; ++ag) {
       for (int ci = 0; ci < (int)caps.size(); ++ci) {
         // ring shards and staged rows / columns sized in proportion to the task
         // counters (typical full-iteration candidates: G ~ 0.19, rows ~ 0.69 of 2 Tf + G)
         int SC = caps[ci];
         int GC = std::max(16, (SC * 5 + 23) / 24);
-        int RC = std::max(64, SC * 11 / 16);
+        int RC = rc_frac ? std::max(64, SC * rc_frac / 16) : 0;
         size_t wb = al16(warp_bytes_of(P, SC, GC, RC, ag));
         int cw = 0, cwp = 0;
-        for (int wp : {8, 7, 6, 5, 4, 3, 2, 1}) {
+        for (int wp : {12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1}) {
+          if (wp * 32 > PS_MAX_THREADS) continue;
           size_t blk = tb + wp * wb;
           if (blk > (size_t)optin) continue;
           int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
-          int warps = std::min(64, blocks * wp);
+          int warps = std::min(reg_warps / wp * wp, blocks * wp);
           if (warps > cw) { cw = warps; cwp = wp; }
         }
         if (cw > bestWarps || (cw >= target && bestWarps < target)) {
