@@ -1236,6 +1236,7 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
     const unsigned long long X_ = (LBBITS) == INF_BITS ? ~0ull : (LBBITS);                   \
     if (!back_refill(w, n, nb, minb, X_, lane)) pend_bslow = true;                           \
     refilled = true;                                                                         \
+    PH_CNT(21, 1);                                                                           \
     continue;                                                                                \
   }
 
@@ -1477,6 +1478,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     int sel_base = 0, sel_n = bslow ? 33 : n, rest = 0;
     bool forced = false;
     if (!bslow && n > 32 && n <= 64 && n + 32 <= w.rcap) {
+      PH_CNT(22, 1);
       bool vA = true, vB = lane + 32 < n;
       unsigned long long hA = w.rs[lane].h, kA = w.rs[lane].k, hB = vB ? w.rs[lane + 32].h : ~0ull,
                          kB = vB ? w.rs[lane + 32].k : ~0ull;
@@ -1688,6 +1690,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       PH_ADD(19, t_slow);
       PH_CNT(18, nw);
     }
+    PH_T(t_run);
     // ---- run the winners: per queue in (ready, origin) order
 #pragma unroll 1
     for (int lv = ran ? 1 : 0; lv <= maxrank; ++lv) {
@@ -1719,6 +1722,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
         w.tr->tasks[myrec] = rec;
       }
     }
+    PH_ADD(20, t_run);
     PH_ADD(2, t_sel);
     TC(7);
     PH_CNT(13, nw);

@@ -34,6 +34,8 @@ print(f"sims={sims} proposals={ph[7]} rounds/sim={rounds/max(sims,1):.1f} avg n=
       f"state in smem={ph[10]/max(sims,1):.2f}")
 print(f"slow rounds {100*ph[16]/max(rounds,1):.1f}% avg n(slow)={ph[17]/max(ph[16],1):.1f} "
       f"winners(slow)={ph[18]/max(ph[16],1):.2f} cycles/slow round={ph[19]/max(ph[16],1):.0f}")
+print(f"run-winners {ph[20]/max(rounds,1):.0f} cycles/round; refill restarts {100*ph[21]/max(rounds,1):.1f}% of rounds; "
+      f"medium-path rounds {100*ph[22]/max(rounds,1):.1f}%")
 tot = ph[6]
 for i in (0, 1, 2, 5, 15, 19, 3, 4):
     print(f"{names[i]:12s} {ph[i]/max(sims,1):12.0f} cycles/sim  {100*ph[i]/max(tot,1):5.1f}% of loop   "
