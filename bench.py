@@ -61,6 +61,8 @@ def parse():
                     help="score every proposal from time zero instead of resuming from a snapshot")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-proposals", type=int, default=1000,
+                    help="CPU arm: proposals per chain, the window the GPU chains cover in the default bench")
     ap.add_argument("--py-ref-seconds", type=float, default=8.0,
                     help="wall time of the Python-reference leg (0: skip)")
     ap.add_argument("--extra", default="alexnet,resnet,nmt,random1k,random10k",
@@ -152,22 +154,34 @@ def profiled_traffic_per_eval():
         return None
 
 
-def cpu_baseline(g, topo, prof, mode, md, init, seeds, seconds, threads):
-    """The oracle (CPU restatement of the reference path) on a bounded sample."""
+def cpu_baseline(g, topo, prof, mode, md, init, seeds, seconds, threads, proposals=1000, first=0):
+    """The oracle (CPU restatement of the reference path) on a bounded sample of
+    the GPU workload: the same chains (starts and seeds, from chain `first` on),
+    each running the same window of `proposals` proposals from its start that the
+    GPU chains run in the bench (chains slow down as their strategies evolve, so
+    the window matters), `threads` chains at a time on all host threads, until
+    `seconds` have passed (each chain also stops at that deadline)."""
     from oracle.oracle_io import Oracle
     orc = Oracle()
-    n = min(len(init), threads)
-    # wall-clock bounded: every chain stops between proposals at the deadline
     t0 = time.perf_counter()
-    out = orc.mcmc(g, topo, prof, mode, init[:n], seeds[:n], 200000, md, rng_mode="philox", threads=threads,
-                   deadline_s=seconds)
+    evals = props = done = 0
+    c = first
+    while done == 0 or time.perf_counter() - t0 < seconds:
+        batch = [(c + j) % len(init) for j in range(threads)]
+        left = seconds - (time.perf_counter() - t0)
+        out = orc.mcmc(g, topo, prof, mode, [init[i] for i in batch], [seeds[i] for i in batch], proposals, md,
+                       rng_mode="philox", threads=threads, deadline_s=max(0.05, left))
+        p = float(out["summary"][:, 2].sum())
+        props += p
+        evals += p + len(batch)  # (the initial full evaluation of each chain counts too)
+        done += len(batch)
+        c += len(batch)
     dt = time.perf_counter() - t0
-    total = float(out["summary"][:, 2].sum())
-    # the initial full evaluation of each chain is counted as an evaluation too
-    evals = total + n
     return {"value": evals / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"{n} chains x {total / n:.0f} proposals on average ({mode}, rebuild+full simulate per "
-                       f"proposal, wall-clock bounded), {dt:.1f}s")}
+            "sample": (f"{done} chains (from chain {first}) x up to {proposals} proposals each, the GPU chains' "
+                       f"window ({props / done:.0f} on average; {mode}, rebuild + full simulate per proposal), "
+                       f"{threads} at a time, {dt:.1f}s"),
+            "next_chain": c}
 
 
 def _py_ref_chain(job):
@@ -216,13 +230,18 @@ def run_reference(args):
     g, topo, md, desc = workload(args.config, args.ops)
     prof = ps.CostProfile()
     threads = os.cpu_count() or 1
-    init = initial_strategies(g, topo, md, 0, threads)
-    seeds = [1000003 * c for c in range(threads)]
+    C = args.chains
+    init = initial_strategies(g, topo, md, 0, C)
+    seeds = [1000003 * c for c in range(C)]
     vals = []
+    nxt = 0
     for i in range(args.warmup + args.steps):
         # warm-up steps are short (1 s); timed steps are wall-clock-bounded samples
+        # that continue through the chain list
         secs = 1.0 if i < args.warmup else max(2.0, args.cpu_seconds / 2)
-        res = cpu_baseline(g, topo, prof, args.mode, md, init, seeds, secs, threads)
+        res = cpu_baseline(g, topo, prof, args.mode, md, init, seeds, secs, threads,
+                           proposals=args.ref_proposals, first=nxt)
+        nxt = res.pop("next_chain")
         if i >= args.warmup:
             vals.append(res["value"])
     v = statistics.mean(vals)
@@ -232,7 +251,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": desc, "mode": args.mode, "max_degree": md, "chains": len(init)},
+            "config": {"workload": desc, "mode": args.mode, "max_degree": md, "chains": len(init),
+                       "proposals_per_chain": args.ref_proposals},
             "cpu_baseline": {**res, "value": v},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -572,8 +592,11 @@ def run_ours(args):
                 line["configs"][name] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        # the GPU chains' window: proposals per chain from their starts to the end of the timed steps
+        window = max(1, round(sum(s.proposals for s in summ) / C))
         line["cpu_baseline"] = cpu_baseline(g, topo, prof, args.mode, md, ch.init, [1000003 * c for c in range(C)],
-                                            args.cpu_seconds, threads)
+                                            args.cpu_seconds, threads, proposals=window)
+        line["cpu_baseline"].pop("next_chain", None)
         py = python_reference(g, topo, args.mode, md, ch.init, args.py_ref_seconds, threads)
         if py is not None:
             line["cpu_baseline"]["python_reference"] = py

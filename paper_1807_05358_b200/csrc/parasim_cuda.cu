@@ -1083,16 +1083,51 @@ __device__ __forceinline__ unsigned long long back_lb(const W2 &w, int nb, int l
 // such boundary is found.
 __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsigned long long &minb,
                                             unsigned long long X, int lane) {
+  // one pass over the ready times: the entries to move (their positions, in
+  // order, while they fit), the minimum of those that stay, and the minimum
+  const int room = w.rcap - n;
+  int *idx = w.mem;  // (the slow path's member list: free between rounds; rcap ints)
+  const unsigned lt = (1u << lane) - 1u;
   int cnt = 0;
-  unsigned long long mn = ~0ull;
+  unsigned long long mn = ~0ull, mnk = ~0ull;
 #pragma unroll 4
-  for (int i = lane; i < nb; i += 32) {
-    unsigned long long h = w.bq[i].h;
-    cnt += h < X ? 1 : 0;
+  for (int base = 0; base < nb; base += 32) {
+    int i = base + lane;
+    unsigned long long h = i < nb ? w.bq[i].h : ~0ull;
+    bool mv = h < X;
+    unsigned bm = __ballot_sync(FULLMASK, mv);
+    int pos = cnt + __popc(bm & lt);
+    if (mv && pos < room) idx[pos] = i;
+    cnt += __popc(bm);
+    if (!mv) mnk = h < mnk ? h : mnk;
     mn = h < mn ? h : mn;
   }
-  cnt = (int)__reduce_add_sync(FULLMASK, (unsigned)cnt);
-  const int room = w.rcap - n;
+  if (cnt <= room && cnt <= 1024) {
+    // few to move (the usual case): copy them out, then fill the holes they
+    // leave below the new end with the survivors of the tail, in order
+    __syncwarp();
+    for (int k = lane; k < cnt; k += 32) w.rs[n + k] = w.bq[idx[k]];
+    const int nb2 = nb - cnt;
+    unsigned *mask = (unsigned *)w.wlane;  // bit t: tail position nb2 + t moved (cnt <= room <= 1024)
+    for (int k = lane; k < (cnt + 31) / 32; k += 32) mask[k] = 0u;
+    __syncwarp();
+    for (int k = lane; k < cnt; k += 32)
+      if (idx[k] >= nb2) atomicOr(&mask[(idx[k] - nb2) >> 5], 1u << ((idx[k] - nb2) & 31));
+    __syncwarp();
+    int carry = 0;
+    for (int tb = 0; tb < cnt; tb += 32) {
+      int t = tb + lane;
+      bool surv = t < cnt && !((mask[t >> 5] >> (t & 31)) & 1u);
+      unsigned bs = __ballot_sync(FULLMASK, surv);
+      if (surv) w.bq[idx[carry + __popc(bs & lt)]] = w.bq[nb2 + t];  // (holes < nb2 <= survivors)
+      carry += __popc(bs);
+    }
+    n += cnt;
+    nb = nb2;
+    minb = warp_min64(mnk, lane);
+    __syncwarp();
+    return true;
+  }
   if (cnt > room) {
     if (X == ~0ull || room < 1) return false;
     mn = warp_min64(mn, lane);
@@ -1144,7 +1179,6 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
   }
   int kept = 0;
   unsigned long long mb = ~0ull;
-  const unsigned lt = (1u << lane) - 1u;
   for (int base = 0; base < nb; base += 32) {
     int i = base + lane;
     bool v = i < nb;
