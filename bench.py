@@ -594,8 +594,12 @@ def run_ours(args):
         threads = os.cpu_count() or 1
         # the GPU chains' window: proposals per chain from their starts to the end of the timed steps
         window = max(1, round(sum(s.proposals for s in summ) / C))
-        line["cpu_baseline"] = cpu_baseline(g, topo, prof, args.mode, md, ch.init, [1000003 * c for c in range(C)],
-                                            args.cpu_seconds, threads, proposals=window)
+        # (in a fresh process: this one holds a CUDA context and its runtime threads)
+        import multiprocessing as mproc
+        with mproc.get_context("spawn").Pool(1) as pool:
+            line["cpu_baseline"] = pool.apply(cpu_baseline, (g, topo, prof, args.mode, md, ch.init,
+                                                             [1000003 * c for c in range(C)], args.cpu_seconds,
+                                                             threads), {"proposals": window})
         line["cpu_baseline"].pop("next_chain", None)
         py = python_reference(g, topo, args.mode, md, ch.init, args.py_ref_seconds, threads)
         if py is not None:
