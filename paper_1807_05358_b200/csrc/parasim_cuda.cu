@@ -2303,25 +2303,15 @@ struct Given {
   int *status;
 };
 
+// One chain's segment of the MCMC (k_mcmc runs the chains of a warp one after another).
 template <int S>
-__global__ void __launch_bounds__(PS_MAX_THREADS, 1)
-k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
-       int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
-       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
-       DeltaBufs db, Given gv) {
+__device__ __forceinline__ void mcmc_chain(const DevProb &P, const Lay &lay, const Tab &T, W2 &w, int lane, int chain,
+                                           int proposals, int rng_mode, int beta_given, double beta_param,
+                                           double ln10, int *maps, unsigned char *asgs, int *best_maps,
+                                           unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
+                                           double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gs,
+                                           unsigned long long budget_ns, const DeltaBufs &db, const Given &gv) {
   constexpr bool DELTA = (S & SIM_SNAP) != 0;
-  extern __shared__ __align__(16) char smem[];
-  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  int chain = blockIdx.x * wpb + wib;
-  char *gs = gscratch + (size_t)(chain < n_chains ? chain : 0) * gslice_bytes(P, lay);
-  Tab T;
-  W2 w;
-  kernel_layout(P, lay, smem, gs, wib, T, w);
-  __syncthreads();
-  if (chain >= n_chains) return;
-  bind_bids(P, gs, w);
-  if (lane == 0) w.flags[0] = 1;
-  __syncwarp();
   int *gmapl = maps + (size_t)chain * P.n_ops;
   unsigned char *gasg = asgs + (size_t)chain * P.n_slots;
   ChainState cs = st[chain];
@@ -2510,6 +2500,35 @@ k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_g
   if (DELTA && lane == 0) db.cd[chain] = w.dc->ch;
 }
 
+template <int S>
+__global__ void __launch_bounds__(PS_MAX_THREADS, 1)
+k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
+       int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
+       double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
+       DeltaBufs db, Given gv) {
+  extern __shared__ __align__(16) char smem[];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
+  char *gs = gscratch + (size_t)(gw < n_chains ? gw : 0) * gslice_bytes(P, lay);
+  Tab T;
+  W2 w;
+  kernel_layout(P, lay, smem, gs, wib, T, w);
+  __syncthreads();
+  if (gw >= n_chains) return;
+  bind_bids(P, gs, w);
+  if (lane == 0) w.flags[0] = 1;
+  __syncwarp();
+  // chains gw, gw + nw, ...: a warp runs its chains one after another when there
+  // are more chains than resident warps (no second wave waiting for the first);
+  // a time-boxed segment is split evenly among them
+  const int m = (n_chains - gw + nw - 1) / nw;
+  const unsigned long long slice = budget_ns ? (budget_ns / (unsigned long long)m > 0 ? budget_ns / m : 1ull) : 0ull;
+#pragma unroll 1
+  for (int chain = gw; chain < n_chains; chain += nw)
+    mcmc_chain<S>(P, lay, T, w, lane, chain, proposals, rng_mode, beta_given, beta_param, ln10, maps, asgs, best_maps,
+                  best_asgs, st, mt_all, trace_cand, trace_ok, trace_cap, gs, slice, db, gv);
+}
+
 __global__ void k_best(const ChainState *st, int n, double *best_cost, int *best_chain) {
   // single block argmin by (best, chain) -- earliest chain wins ties (search.py:256)
   __shared__ double sb[1024];
@@ -2626,6 +2645,7 @@ struct ps_mcmc {
   DeltaBufs db;  // delta-evaluation state (db.cd == nullptr: every proposal simulates from scratch)
   char *given = nullptr;  // ps_delta_batch staging (host-pointer calls)
   size_t given_bytes = 0;
+  int max_blocks = 0;     // PS_MCMC_MUX: resident blocks of the handle's k_mcmc variant (0: not yet known)
 };
 
 static int ensure_io(ps_problem *pr, size_t n) {
@@ -3275,6 +3295,20 @@ static int mcmc_launch(ps_mcmc *m, int proposals, unsigned long long budget_ns, 
   int blocks = (m->n + wpb - 1) / wpb;
   size_t smem = pr->smem_per_block;
   auto km = mcmc_kernel(!pr->simple ? 0 : pr->P.full ? 1 : 2, m->db.cd != nullptr, pr->wide);
+  // One warp per chain: chains beyond one resident wave wait for a block to
+  // finish (the block scheduler balances fast and slow chains).  PS_MCMC_MUX caps
+  // the grid at one resident wave instead, each warp running its chains in turn
+  // with the time box split among them -- measured slower on wide problems
+  // (NMT-40, 4096 chains: 10k vs 42k proposals per 300 ms step), where a warp
+  // with slow chains holds the whole launch.
+  if (getenv("PS_MCMC_MUX")) {
+    if (m->max_blocks <= 0) {
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, km, wpb * 32, smem));
+      m->max_blocks = std::max(1, occ) * pr->sm_count;
+    }
+    blocks = std::min(blocks, m->max_blocks);
+  }
   km<<<blocks, wpb * 32, smem, (cudaStream_t)stream>>>(
       pr->P, pr->lay, m->n, proposals, m->params.rng_mode, m->params.beta_given, m->params.beta, m->params.ln10, m->maps,
       m->asgs, m->best_maps, m->best_asgs, m->st, m->mt, m->trace_cand, m->trace_ok,

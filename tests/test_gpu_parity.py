@@ -714,3 +714,56 @@ def test_two_level_ready_set_matches_oracle(oracle, monkeypatch, cap, warp_globa
             assert [(s.initial_cost, s.best_cost, s.proposals, s.accepted) for s in a] == \
                 [tuple(r[:4]) for r in ref["summary"]], (mode, cap)
             assert np.array_equal(at, ref["cand"])
+
+
+@pytest.mark.parametrize("budget,mux", [(False, False), (True, False), (False, True), (True, True)])
+def test_more_chains_than_resident_warps(oracle, monkeypatch, budget, mux):
+    """More chains than resident warps: later blocks wait for a resident one to
+    finish, or (PS_MCMC_MUX) the resident warps run their chains in turn with
+    the time box split among them.  Every chain's summary and trace equal the
+    oracle's for the proposals it made."""
+    if mux:
+        monkeypatch.setenv("PS_MCMC_MUX", "1")
+    import ctypes
+    from paper_1807_05358_b200 import _native as nat
+    from paper_1807_05358_b200.lowering import lower
+    g, topo, md = ps.alexnet_like(), ps.single_node_topology(4), 4
+    prof = ps.CostProfile()
+    C = 2600
+    init = [ps.data_parallel_strategy(g, topo)] + ps.random_strategies(g, topo, md, list(range(1, C)))
+    seeds = [11 + 1000003 * c for c in range(C)]
+    low = lower(g, topo, prof, ps.MODE_FULL, max_degree=md, strategies=init)
+    assert low.info().resident_warps_per_sm * 148 < C
+    maps = np.zeros((C, low.n_ops), dtype=np.int32)
+    asg = np.zeros((C, low.n_slots), dtype=np.uint8)
+    for i, s in enumerate(init):
+        low.encode(s, maps[i], asg[i])
+    L = nat.lib()
+    P = 40
+    mp = nat.PsMcmcParams(nat.PS_RNG_PHILOX, 0, 0.0, math.log(10.0), 1, P, 1)
+    h = ctypes.c_void_p()
+    sd = np.array(seeds, dtype=np.uint64)
+    nat.check(L.ps_mcmc_create(low.handle(), ctypes.byref(mp), C, nat.ptr(maps), nat.ptr(asg), nat.ptr(sd), None,
+                               ctypes.byref(h)), "ps_mcmc_create")
+    try:
+        if budget:
+            nat.check(L.ps_mcmc_run_budget(h, P, 2_000_000, None), "ps_mcmc_run_budget")  # 2 ms, split per warp
+        else:
+            nat.check(L.ps_mcmc_run(h, P, None), "ps_mcmc_run")
+        summ = (nat.PsChainSummary * C)()
+        tc = np.zeros((C, P))
+        nat.check(L.ps_mcmc_read(h, summ, None, None, nat.ptr(tc), None), "ps_mcmc_read")
+    finally:
+        L.ps_mcmc_destroy(h)
+    counts = sorted({s.proposals for s in summ})
+    assert counts[-1] > 0 and all(s.status == nat.PS_STATUS_OK for s in summ)
+    if not budget:
+        assert counts == [P]
+    for p in counts:
+        idx = [c for c in range(C) if summ[c].proposals == p][:64]  # a sample per proposal count
+        ref = oracle.mcmc(g, topo, prof, ps.MODE_FULL, [init[c] for c in idx], [seeds[c] for c in idx], p, md,
+                          rng_mode="philox", threads=8)
+        for j, c in enumerate(idx):
+            s = summ[c]
+            assert (s.initial_cost, s.best_cost, s.proposals, s.accepted) == tuple(ref["summary"][j][:4]), (c, p)
+            assert list(tc[c, :p]) == list(ref["cand"][j, :p]), (c, p)
