@@ -98,6 +98,7 @@ struct DevProb {
   // prefix-reuse argument does not hold and every evaluation runs from scratch)
   int n_rings;
   double min_exe;
+  int snap_b;  // back-set entries a snapshot can hold (wide problems; 0: snapshots need an empty back set)
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(unsigned kind, unsigned a, unsigned b,
@@ -366,7 +367,7 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15
 
 // per-warp phase counters of -DPS_PHASES builds (16 bytes otherwise)
 #ifdef PS_PHASES
-#define PH_N 24
+#define PH_N 32
 #else
 #define PH_N 2
 #endif
@@ -397,14 +398,16 @@ struct __align__(16) SnapHdr {
   int round, n, Tf, G;
   double makespan;
   int valid, epoch;        // epoch: in-degree buffer of the strategy that wrote it
-  int pad_[8];
+  int nb, pad0_;           // back-set entries (wide problems)
+  unsigned long long minb; // their lower bound
+  int pad_[4];
 };
 
 // Snapshot layout: header, dense layout (fbase / gbase), queue clocks, ready set,
 // and the raw dense counters (remaining count, ready time).  Arrivals are
 // in-degree minus remaining, with the in-degrees of the writing strategy kept
 // in a per-chain epoch buffer (written once per simulation, by its init).
-struct SnapLay { size_t fb, gb, qc, rs, rm, rd, total; };
+struct SnapLay { size_t fb, gb, qc, rs, rm, rd, rb, total; };
 
 __host__ __device__ inline size_t snap_counters(const DevProb &P) {
   return P.full ? 2 * (size_t)P.n_slots + (size_t)P.n_rings : (size_t)P.n_slots;
@@ -421,6 +424,7 @@ __host__ __device__ inline SnapLay snap_layout(const DevProb &P) {
   L.rs = o; o += al16(32 * (size_t)P.cap);
   L.rm = o; o += al16(2 * snap_counters_pad(P));
   L.rd = o; o += al16(8 * snap_counters_pad(P));
+  L.rb = o; o += al16(32 * (size_t)P.snap_b);
   L.total = al16(o);
   return L;
 }
@@ -1002,19 +1006,21 @@ __device__ __forceinline__ void copy16(void *dst, const void *src, size_t bytes,
 // Snapshot of the simulation state at the start of round `round` (index i):
 // vector copies of the dense layout, queue clocks, ready set and raw counters.
 // A ready set larger than a snapshot holds marks the index unusable.
-__device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const State &st, int n, int round, int i,
-                                           double mk, bool full, int lane) {
+__device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const State &st, int n, int nb,
+                                           unsigned long long minb, int round, int i, double mk, bool full,
+                                           int lane) {
   DeltaCtx *dc = w.dc;
   const SnapLay sl = snap_layout(P);
   char *dst = dc->snap + (2ull * (unsigned)i + ((dc->out_sel >> i) & 1u)) * dc->snap_bytes;
   const int nc = full ? 2 * st.Tf + st.G : st.Tf;
-  bool ok = n <= P.cap;
+  bool ok = n <= P.cap && nb <= P.snap_b;
   unsigned long long mb = (unsigned long long)__double_as_longlong(mk);
   unsigned hi = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32));
   unsigned lo = __reduce_max_sync(FULLMASK, (unsigned)(mb >> 32) == hi ? (unsigned)mb : 0u);
   if (lane == 0) {
     SnapHdr h;
     h.round = round; h.n = n; h.Tf = st.Tf; h.G = st.G; h.valid = ok; h.epoch = dc->epoch;
+    h.nb = nb; h.pad0_ = 0; h.minb = minb;
     h.makespan = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
     *(SnapHdr *)dst = h;
     dc->last = i;
@@ -1026,14 +1032,14 @@ __device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const 
   // with a count of 0xffff meanwhile; the raw copy below is taken before)
   copy16(dst + sl.rm, st.rem, 2 * (size_t)nc, lane);
   __syncwarp();
-  for (int j = lane; j < n; j += 32) {
-    unsigned kd = key_kind(w.rs[j].k);
-    if (kd == KIND_OP || kd == KIND_OP_BWD)
-      st.rem[(kd == KIND_OP ? 0 : st.Tf) + w.fbase[key_a(w.rs[j].k)] + key_c(w.rs[j].k)] = 0xffff;
+  for (int j = lane; j < n + nb; j += 32) {
+    const unsigned long long k = j < n ? w.rs[j].k : w.bq[j - n].k;
+    unsigned kd = key_kind(k);
+    if (kd == KIND_OP || kd == KIND_OP_BWD) st.rem[(kd == KIND_OP ? 0 : st.Tf) + w.fbase[key_a(k)] + key_c(k)] = 0xffff;
   }
   __syncwarp();
-  const int nb = full ? 2 : 1;
-  for (int x = lane; x < nb * P.n_ops; x += 32) {
+  const int ndir = full ? 2 : 1;
+  for (int x = lane; x < ndir * P.n_ops; x += 32) {
     if (w.ran[x]) continue;
     int o = x < P.n_ops ? x : x - P.n_ops;
     int base = (x < P.n_ops ? 0 : st.Tf) + w.fbase[o], sz = w.fbase[o + 1] - w.fbase[o];
@@ -1045,16 +1051,17 @@ __device__ __forceinline__ void snap_write(const DevProb &P, const W2 &w, const 
     }
   }
   __syncwarp();
-  for (int j = lane; j < n; j += 32) {
-    unsigned kd = key_kind(w.rs[j].k);
-    if (kd == KIND_OP || kd == KIND_OP_BWD)
-      st.rem[(kd == KIND_OP ? 0 : st.Tf) + w.fbase[key_a(w.rs[j].k)] + key_c(w.rs[j].k)] = 0;
+  for (int j = lane; j < n + nb; j += 32) {
+    const unsigned long long k = j < n ? w.rs[j].k : w.bq[j - n].k;
+    unsigned kd = key_kind(k);
+    if (kd == KIND_OP || kd == KIND_OP_BWD) st.rem[(kd == KIND_OP ? 0 : st.Tf) + w.fbase[key_a(k)] + key_c(k)] = 0;
   }
   __syncwarp();
   copy16(dst + sl.fb, w.fbase, 4 * (size_t)(P.n_ops + 1), lane);
   if (full) copy16(dst + sl.gb, w.gbase, 4 * (size_t)(P.n_ops + 1), lane);
   copy16(dst + sl.qc, w.qclock, 8 * (size_t)P.n_queues, lane);
   copy16(dst + sl.rs, w.rs, 32 * (size_t)n, lane);
+  if (nb) copy16(dst + sl.rb, w.bq, 32 * (size_t)nb, lane);
   copy16(dst + sl.rd, st.ready, 8 * (size_t)nc, lane);
 }
 
@@ -1425,9 +1432,15 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     for (int q = lane; q < P.n_queues; q += 32) w.qclock[q] = qco[q];
     n = hd->n;
     const REnt *rso = (const REnt *)(src + sl.rs);
-    for (int i = lane; i < n; i += 32) {
-      REnt r = rso[i];
-      w.rs[i] = r;
+    const REnt *rbo = (const REnt *)(src + sl.rb);
+    if (BACK) {
+      nb = hd->nb;
+      minb = hd->minb;
+    }
+    for (int i = lane; i < n + nb; i += 32) {
+      REnt r = i < n ? rso[i] : rbo[i - n];
+      if (i < n) w.rs[i] = r;
+      else w.bq[i - n] = r;
       // a ready op task has no remaining count (the snapshots' "has run" test
       // reads it: ran = no remaining count and not in the ready set)
       unsigned kd = key_kind(r.k);
@@ -1463,7 +1476,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   while (n > 0 || (BACK && nb > 0)) {
     if (SNAP && round == next_snap) {
       // (a state with a back set is not snapshotted: the index is marked unusable)
-      snap_write(P, w, st, nb ? P.cap + 1 : n, round, round / w.dc->stride, out.makespan, FULL, lane);
+      PH_CNT(23, 1);
+      PH_CNT(24, nb > P.snap_b ? 1 : 0);
+      PH_CNT(25, n > P.cap ? 1 : 0);
+      snap_write(P, w, st, n, nb, minb, round, round / w.dc->stride, out.makespan, FULL, lane);
       next_snap = round / w.dc->stride + 1 < w.dc->nsnap ? round + w.dc->stride : 0x7fffffff;
     }
     PH_T(t_sel);
@@ -2765,6 +2781,8 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
         if (i != j && d->link_of[i * P.n_dev + j] < 0) { mesh = false; break; }
     pr->simple = mesh && P.n_cls > 0 && P.n_kinds == 1;
     pr->wide = P.n_slots >= 4096 || getenv("PS_FORCE_WIDE") != nullptr;
+    // delta snapshots of wide problems also hold the back ready set (up to 1024 entries)
+    P.snap_b = pr->wide ? std::min(overflow_cap(P.n_slots), 1024) : 0;
     std::vector<short> l16((size_t)P.n_dev * P.n_dev);
     for (size_t i = 0; i < l16.size(); ++i) {
       int li = d->link_of[i];
@@ -3253,11 +3271,12 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     // delta evaluation: snapshots per chain (two copies per index), first
     // rounds, in-degrees.  Off when some task can take zero time, when asked
     // (params->delta == 0 / PS_NO_DELTA), or when fewer than 4 snapshot indices
-    // fit in a quarter of the free device memory (8 GiB at most).
+    // fit in a quarter of the device memory.
     size_t sb = snap_layout(P).total;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    size_t budget = std::min((size_t)8 << 30, total_b / 16);
+    size_t budget = total_b / 4;
+    if (const char *e = getenv("PS_SNAP_BUDGET_GB")) budget = std::min(total_b / 3, (size_t)atof(e) * ((size_t)1 << 30));
     // snapshot indices per chain: more resume points vs more snapshot writes per
     // simulation (measured on Inception-v3 4x4: full-iteration 8 > 12 > 24,
     // forward 12 > 8 > 24)

@@ -16,7 +16,7 @@ distinct = None if cfg in ("inception", "alexnet", "resnet") else 16
 ch = Chains(cfg, mode, C, 0, True, 0, distinct=distinct)
 L = nat.lib()
 L.ps_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_int]
-N = 24
+N = 32
 ph = np.zeros(N, np.uint64)
 nat.check(L.ps_mcmc_run_budget(ch.h, 1 << 30, int(bms * 0.5e6), None), "run")
 nat.check(L.ps_debug_phases(nat.ptr(ph), 1), "phases")
@@ -36,6 +36,8 @@ print(f"slow rounds {100*ph[16]/max(rounds,1):.1f}% avg n(slow)={ph[17]/max(ph[1
       f"winners(slow)={ph[18]/max(ph[16],1):.2f} cycles/slow round={ph[19]/max(ph[16],1):.0f}")
 print(f"run-winners {ph[20]/max(rounds,1):.0f} cycles/round; refill restarts {100*ph[21]/max(rounds,1):.1f}% of rounds; "
       f"medium-path rounds {100*ph[22]/max(rounds,1):.1f}%")
+print(f"snapshots {ph[23]/max(sims,1):.1f}/sim, unusable: back set {100*ph[24]/max(ph[23],1):.1f}% "
+      f"ready set over capacity {100*ph[25]/max(ph[23],1):.1f}%")
 tot = ph[6]
 for i in (0, 1, 2, 5, 15, 19, 3, 4):
     print(f"{names[i]:12s} {ph[i]/max(sims,1):12.0f} cycles/sim  {100*ph[i]/max(tot,1):5.1f}% of loop   "
