@@ -2638,6 +2638,13 @@ struct ps_problem {
     double *d_best = nullptr;
     int *d_bestc = nullptr;
   } spare;
+  struct {  // delta buffers kept from the last destroyed MCMC handle (same chain and snapshot counts)
+    int n = 0, ns = 0;
+    ChainDelta *cd = nullptr;
+    char *snaps = nullptr;
+    int *frb = nullptr;
+    unsigned short *indeg = nullptr;
+  } spare_delta;
   size_t io_cap = 0;
   long long device_bytes = 0;
   std::vector<int> h_map_off, h_map_size;  // host copies: argument checks of ps_delta_batch
@@ -3009,6 +3016,8 @@ void ps_problem_destroy(ps_problem *pr) {
   cudaFree(pr->mcmc_scratch);
   cudaFree(pr->spare.maps); cudaFree(pr->spare.best_maps); cudaFree(pr->spare.asgs); cudaFree(pr->spare.best_asgs);
   cudaFree(pr->spare.st); cudaFree(pr->spare.d_best); cudaFree(pr->spare.d_bestc);
+  cudaFree(pr->spare_delta.cd); cudaFree(pr->spare_delta.snaps); cudaFree(pr->spare_delta.frb);
+  cudaFree(pr->spare_delta.indeg);
   delete pr;
 }
 
@@ -3293,12 +3302,19 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
         CK(cudaMemset(m->db.dbg, 0xff, (size_t)n * m->db.dbg_cap * 8 * sizeof(int)));
       }
       m->db.snap_bytes = sb;
-      CK(cudaMalloc(&m->db.cd, (size_t)n * sizeof(ChainDelta)));
+      if (pr->spare_delta.cd && pr->spare_delta.n == n && pr->spare_delta.ns == ns) {
+        // reuse (create / run / destroy cycles allocate nothing)
+        m->db.cd = pr->spare_delta.cd; m->db.snaps = pr->spare_delta.snaps; m->db.frb = pr->spare_delta.frb;
+        m->db.indeg = pr->spare_delta.indeg;
+        pr->spare_delta.cd = nullptr; pr->spare_delta.n = 0;
+      } else {
+        CK(cudaMalloc(&m->db.cd, (size_t)n * sizeof(ChainDelta)));
+        CK(cudaMalloc(&m->db.snaps, (size_t)n * 2 * ns * sb));
+        CK(cudaMalloc(&m->db.frb, (size_t)n * 4 * P.n_ops * sizeof(int)));
+        CK(cudaMalloc(&m->db.indeg, (size_t)n * (ns + 1) * snap_counters_pad(P) * sizeof(unsigned short)));
+      }
       CK(cudaMemset(m->db.cd, 0, (size_t)n * sizeof(ChainDelta)));
-      CK(cudaMalloc(&m->db.snaps, (size_t)n * 2 * ns * sb));
-      CK(cudaMalloc(&m->db.frb, (size_t)n * 4 * P.n_ops * sizeof(int)));
       CK(cudaMemset(m->db.frb, 0x7f, (size_t)n * 4 * P.n_ops * sizeof(int)));  // "never ran"
-      CK(cudaMalloc(&m->db.indeg, (size_t)n * (ns + 1) * snap_counters_pad(P) * sizeof(unsigned short)));
       CK(cudaMemset(m->db.indeg, 0, (size_t)n * (ns + 1) * snap_counters_pad(P) * sizeof(unsigned short)));
     }
   }
@@ -3526,7 +3542,13 @@ void ps_mcmc_destroy(ps_mcmc *m) {
     cudaFree(m->d_best); cudaFree(m->d_bestc);
   }
   cudaFree(m->mt); cudaFree(m->trace_cand); cudaFree(m->trace_ok); cudaFree(m->given);
-  cudaFree(m->db.dbg); cudaFree(m->db.cd); cudaFree(m->db.snaps); cudaFree(m->db.frb); cudaFree(m->db.indeg);
+  cudaFree(m->db.dbg);
+  if (m->db.cd && !pr->spare_delta.cd) {  // keep the delta buffers for the problem's next handle
+    pr->spare_delta.n = m->n; pr->spare_delta.ns = m->db.nsnap; pr->spare_delta.cd = m->db.cd;
+    pr->spare_delta.snaps = m->db.snaps; pr->spare_delta.frb = m->db.frb; pr->spare_delta.indeg = m->db.indeg;
+  } else {
+    cudaFree(m->db.cd); cudaFree(m->db.snaps); cudaFree(m->db.frb); cudaFree(m->db.indeg);
+  }
   if (m->scratch) {  // keep the largest chain scratch for the problem's next handle
     if (m->scratch_bytes >= m->prob->mcmc_scratch_bytes) {
       cudaFree(m->prob->mcmc_scratch);
