@@ -414,7 +414,13 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     C = args.chains
-    first = rank * C
+    # weak scaling: C chains per rank, rank r owning the contiguous block
+    # parallel.shard(r, world, world * C) = [r C, (r + 1) C) -- the same split the
+    # API's SearchParams(devices=[...]) uses
+    from paper_1807_05358_b200.parallel import shard
+    blk = shard(rank, world, world * C)
+    first = blk.start
+    assert len(blk) == C
     ch = Chains(args.config, args.mode, C, first, not args.no_delta, local, ops=args.ops)
     L, low, g, topo, md, desc, prof = ch.L, ch.low, ch.g, ch.topo, ch.md, ch.desc, ch.prof
     info = low.info()

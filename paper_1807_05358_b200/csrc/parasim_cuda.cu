@@ -2648,6 +2648,7 @@ struct ps_problem {
   size_t io_cap = 0;
   long long device_bytes = 0;
   std::vector<int> h_map_off, h_map_size;  // host copies: argument checks of ps_delta_batch
+  size_t total_mem = 0;                    // device memory (snapshot budget), queried once
 };
 
 struct ps_mcmc {
@@ -3282,8 +3283,11 @@ int ps_mcmc_create(ps_problem *pr, const ps_mcmc_params *params, int n, const in
     // (params->delta == 0 / PS_NO_DELTA), or when fewer than 4 snapshot indices
     // fit in a quarter of the device memory.
     size_t sb = snap_layout(P).total;
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (!pr->total_mem) {
+      size_t free_b = 0;
+      CK(cudaMemGetInfo(&free_b, &pr->total_mem));
+    }
+    const size_t total_b = pr->total_mem;
     size_t budget = total_b / 4;
     if (const char *e = getenv("PS_SNAP_BUDGET_GB")) budget = std::min(total_b / 3, (size_t)atof(e) * ((size_t)1 << 30));
     // snapshot indices per chain: more resume points vs more snapshot writes per
