@@ -162,6 +162,13 @@ def cpu_baseline(g, topo, prof, mode, md, init, seeds, seconds, threads, proposa
     the window matters), `threads` chains at a time on all host threads, until
     `seconds` have passed (each chain also stops at that deadline)."""
     from oracle.oracle_io import Oracle
+    try:  # (a process that initialised CUDA may have been pinned to the GPU's NUMA node)
+        before = len(os.sched_getaffinity(0))
+        os.sched_setaffinity(0, range(os.cpu_count() or 1))
+        if os.environ.get("PS_BENCH_VERBOSE"):
+            print(f"cpu_baseline: affinity {before} -> {len(os.sched_getaffinity(0))} cpus", file=sys.stderr)
+    except (AttributeError, OSError):
+        pass
     orc = Oracle()
     t0 = time.perf_counter()
     evals = props = done = 0
@@ -397,6 +404,7 @@ def measure_extra(name, mode, device, stream, sh, flush, peak, steps=3, warmup=2
 def run_ours(args):
     import torch
     import torch.distributed as dist
+    import paper_1807_05358_b200 as ps
     from paper_1807_05358_b200 import _native as nat
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -603,7 +611,9 @@ def run_ours(args):
         # (in a fresh process: this one holds a CUDA context and its runtime threads)
         import multiprocessing as mproc
         with mproc.get_context("spawn").Pool(1) as pool:
-            line["cpu_baseline"] = pool.apply(cpu_baseline, (g, topo, prof, args.mode, md, ch.init,
+            # (a fresh profile: `prof` now caches every lowered map's analytic time, which
+            # the oracle would take as explicit overrides and look up more slowly)
+            line["cpu_baseline"] = pool.apply(cpu_baseline, (g, topo, ps.CostProfile(), args.mode, md, ch.init,
                                                              [1000003 * c for c in range(C)], args.cpu_seconds,
                                                              threads), {"proposals": window})
         line["cpu_baseline"].pop("next_chain", None)
