@@ -1375,6 +1375,8 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
   unsigned long long minb = ~0ull;  // lower bound of the back set's ready times (bits; ~0: empty)
   bool okc = true;
   int round = 0, next_snap = 0x7fffffff;  // (SNAP) round counter, round of the next snapshot
+  PH_ADD(26, t_init);
+  PH_T(t_rest);
   if (SNAP && w.dc->restore) {
     // resume: every counter some arrival had touched and that can still be
     // read (a task still waiting on predecessors; every ring: its slot keeps
@@ -1471,6 +1473,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     if (lane == 0) { w.dc->last = w.dc->restore_idx; w.dc->bad = 0; }
   }
   __syncwarp();
+  PH_ADD(27, t_rest);
   PH_ADD(1, t_init);
   if (!okc) { out.status = PS_STATUS_CAPACITY; return out; }
   while (n > 0 || (BACK && nb > 0)) {

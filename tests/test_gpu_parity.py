@@ -679,7 +679,7 @@ def test_sharded_evaluation_equals_one_launch():
     assert list(a) == list(b)
 
 
-@pytest.mark.parametrize("cap,warp_global", [(2, False), (8, True), (128, False), (128, True)])
+@pytest.mark.parametrize("cap,warp_global", [(2, False), (8, True), (128, False), (128, True), (16, "all")])
 def test_two_level_ready_set_matches_oracle(oracle, monkeypatch, cap, warp_global):
     """The wide-problem variants (front ready set in shared memory, unsorted
     back set in global memory with a lower bound on its ready times, refill /
@@ -689,7 +689,9 @@ def test_two_level_ready_set_matches_oracle(oracle, monkeypatch, cap, warp_globa
     from paper_1807_05358_b200.lowering import lower
     from paper_1807_05358_b200.search import _eval_encoded
     monkeypatch.setenv("PS_FORCE_WIDE", "1")
-    if warp_global:  # warp slices in global memory, per-round state in shared memory
+    if warp_global == "all":  # block tables and warp slices in global memory
+        monkeypatch.setenv("PS_FORCE_GLOBAL_ALL", "1")
+    elif warp_global:  # warp slices in global memory, per-round state in shared memory
         monkeypatch.setenv("PS_FORCE_WARP_GLOBAL", "1")
     rng = random.Random(cap)
     cases = [(ps.nmt_like(steps=8, layers=2, batch=64, hidden=64, vocab=64), ps.multi_node_topology(4, 4), 8),
