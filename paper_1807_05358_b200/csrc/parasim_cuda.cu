@@ -1482,7 +1482,9 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       PH_CNT(23, 1);
       PH_CNT(24, nb > P.snap_b ? 1 : 0);
       PH_CNT(25, n > P.cap ? 1 : 0);
+      PH_T(t_snap);
       snap_write(P, w, st, n, nb, minb, round, round / w.dc->stride, out.makespan, FULL, lane);
+      PH_ADD(28, t_snap);
       next_snap = round / w.dc->stride + 1 < w.dc->nsnap ? round + w.dc->stride : 0x7fffffff;
     }
     PH_T(t_sel);
@@ -2420,7 +2422,9 @@ __device__ __forceinline__ void mcmc_chain(const DevProb &P, const Lay &lay, con
       for (int pass = 0; pass < npass; ++pass) {
         if (DELTA) {
           const bool full = (S & SIM_FULL) ? true : (S & SIM_FWD) ? false : P.full != 0;
+          PH_T(t_prep);
           dj = delta_prepare(P, T, w, db, chain, o, cs.cost, full, it < 0, lane);
+          PH_ADD(29, t_prep);
         }
         so = simulate_any<S>(P, T, w, lay, gs, lane);
         if (so.status != PS_STATUS_OK) break;

@@ -1,4 +1,4 @@
 # Round-end check: driver steps (tests, smoke, both bench arms) + API microbench + ncu summaries.
 bash scripts/gpu_round_end.sh
-bash scripts/gpu_prof_r2b.sh > /dev/null 2>&1
+bash scripts/gpu_prof_summaries.sh > /dev/null 2>&1
 ls gpurun_out

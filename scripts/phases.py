@@ -39,6 +39,7 @@ print(f"run-winners {ph[20]/max(rounds,1):.0f} cycles/round; refill restarts {10
 print(f"snapshots {ph[23]/max(sims,1):.1f}/sim, unusable: back set {100*ph[24]/max(ph[23],1):.1f}% "
       f"ready set over capacity {100*ph[25]/max(ph[23],1):.1f}%")
 print(f"init: in-degrees {ph[26]/max(sims,1):.0f} cycles/sim, restore or seed {ph[27]/max(sims,1):.0f} cycles/sim")
+print(f"snapshot writes {ph[28]/max(sims,1):.0f} cycles/sim, delta_prepare {ph[29]/max(sims,1):.0f} cycles/sim")
 tot = ph[6]
 for i in (0, 1, 2, 5, 15, 19, 3, 4):
     print(f"{names[i]:12s} {ph[i]/max(sims,1):12.0f} cycles/sim  {100*ph[i]/max(tot,1):5.1f}% of loop   "
