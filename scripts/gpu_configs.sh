@@ -1,6 +1,6 @@
 # Bench lines for the non-headline BASELINE configs (parity is covered by the tests).
-for cfg in alexnet resnet nmt random; do
-  PS_DEBUG=1 timeout 900 python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline "$@" 2>&1 | grep -E "^\[parasim\]|^\{" | tail -2 | python -c "
+for cfg in alexnet resnet nmt random1k random10k; do
+  PS_DEBUG=1 timeout 900 python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --py-ref-seconds 0 --extra none "$@" 2>&1 | grep -E "^\[parasim\]|^\{" | tail -2 | python -c "
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
