@@ -45,6 +45,16 @@
 #ifndef PS_MAX_THREADS
 #define PS_MAX_THREADS 256
 #endif
+// wide-problem (SIM_BACK) variants: threads per block and blocks per SM they are
+// compiled for.  Their warps wait on global memory (back set, counters of big
+// layouts), so more resident warps pay where they do not on the headline shape.
+#ifndef PS_WIDE_THREADS
+#define PS_WIDE_THREADS PS_MAX_THREADS
+#endif
+#ifndef PS_WIDE_MINB
+#define PS_WIDE_MINB 1
+#endif
+#define PS_BOUNDS(S) __launch_bounds__(((S) & SIM_BACK) ? PS_WIDE_THREADS : PS_MAX_THREADS, ((S) & SIM_BACK) ? PS_WIDE_MINB : 1)
 
 namespace {
 
@@ -2005,7 +2015,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
 }
 
 template <int S>
-__global__ void __launch_bounds__(PS_MAX_THREADS, 1)
+__global__ void PS_BOUNDS(S)
 k_simulate_batch(DevProb P, Lay lay, const int *__restrict__ maps, const unsigned char *__restrict__ asgs, int n,
                  double *makespan, int *status, char *gscratch, double *opmin, int *next) {
   extern __shared__ __align__(16) char smem[];
@@ -2524,7 +2534,7 @@ __device__ __forceinline__ void mcmc_chain(const DevProb &P, const Lay &lay, con
 }
 
 template <int S>
-__global__ void __launch_bounds__(PS_MAX_THREADS, 1)
+__global__ void PS_BOUNDS(S)
 k_mcmc(DevProb P, Lay lay, int n_chains, int proposals, int rng_mode, int beta_given, double beta_param, double ln10,
        int *maps, unsigned char *asgs, int *best_maps, unsigned char *best_asgs, ChainState *st, unsigned *mt_all,
        double *trace_cand, unsigned char *trace_ok, int trace_cap, char *gscratch, unsigned long long budget_ns,
@@ -2903,9 +2913,10 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     if (const char *e = getenv("PS_RC_FRAC")) rc_frac = std::max(0, atoi(e));
     // resident warps per SM the evaluation kernels' registers allow
     int reg_warps = 64;
+    const int max_wpb = (pr->wide ? PS_WIDE_THREADS : PS_MAX_THREADS) / 32;
     {
       cudaFuncAttributes fa;
-      if (cudaFuncGetAttributes(&fa, mcmc_kernel(1, true, false)) == cudaSuccess && fa.numRegs > 0) {
+      if (cudaFuncGetAttributes(&fa, mcmc_kernel(1, true, pr->wide)) == cudaSuccess && fa.numRegs > 0) {
         int per_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
         reg_warps = 65536 / per_warp;
       }
@@ -2920,7 +2931,7 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
         size_t wb = al16(warp_bytes_of(P, SC, GC, RC, ag));
         int cw = 0, cwp = 0;
         for (int wp : {12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1}) {
-          if (wp * 32 > PS_MAX_THREADS) continue;
+          if (wp > max_wpb) continue;
           size_t blk = tb + wp * wb;
           if (blk > (size_t)optin) continue;
           int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
@@ -2944,11 +2955,11 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
       pr->lay.RC = 0;
       pr->lay.tab_bytes = 0;
       pr->lay.warp_bytes = al16(warp_bytes_of(P, pr->lay.SC, pr->lay.GC, pr->lay.RC, 1));
-      pr->wpb = 8;
+      pr->wpb = std::min(8, max_wpb);
       pr->lay.hot_bytes = (int)al16(hot_bytes_of(P));
       if ((size_t)pr->wpb * pr->lay.hot_bytes > (size_t)optin || getenv("PS_NO_HOT")) pr->lay.hot_bytes = 0;
       pr->smem_per_block = (size_t)pr->wpb * pr->lay.hot_bytes;
-      bestW = 8; bestWarps = 8; bestSC = pr->lay.SC;
+      bestW = pr->wpb; bestWarps = std::min(reg_warps, 32); bestSC = pr->lay.SC;
     } else {
       pr->lay.global_all = 0;
       pr->lay.hot_bytes = 0;
@@ -2963,16 +2974,16 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     pr->smem_per_block = tb + bestW * pr->lay.warp_bytes;
     // Wide problems whose warp slices keep few warps resident: the slices move
     // to global memory and only the per-round state stays on chip, when that at
-    // least doubles the resident warps (8 at most: 254 registers per thread)
+    // least doubles the resident warps (as many as the registers allow)
     const bool force_wg = getenv("PS_FORCE_WARP_GLOBAL") != nullptr;  // test hook
     if (pr->wide && (bestWarps < target || force_wg) && !getenv("PS_NO_WARP_GLOBAL")) {
       size_t hot = al16(hot_bytes_of(P));
       int cw = 0, cwp = 0;
       for (int wp : {8, 4, 2}) {
         size_t blk = tb + wp * hot;
-        if (blk > (size_t)optin) continue;
+        if (blk > (size_t)optin || wp > max_wpb) continue;
         int blocks = std::min(32, (int)(per_sm / (blk + 1024)));
-        int warps = std::min(8, blocks * wp);
+        int warps = std::min(reg_warps / wp * wp, blocks * wp);
         if (warps > cw) { cw = warps; cwp = wp; }
       }
       if (cw >= 2 * bestWarps || (force_wg && cw > 0)) {
@@ -3001,7 +3012,8 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     }
   CK(cudaFuncSetAttribute(k_simulate_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_batch<0>, pr->wpb * 32, pr->smem_per_block));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mcmc_kernel(pr->simple ? (P.full ? 1 : 2) : 0, true, pr->wide),
+                                                   pr->wpb * 32, pr->smem_per_block));
   if (getenv("PS_DEBUG"))
     fprintf(stderr, "[parasim] tab=%zu warp=%zu SC=%d GC=%d RC=%d wpb=%d smem/block=%zu occ=%d optin=%d per_sm=%d\n",
             pr->lay.tab_bytes, pr->lay.warp_bytes, pr->lay.SC, pr->lay.GC, pr->lay.RC, pr->wpb, pr->smem_per_block, occ,
