@@ -2807,7 +2807,11 @@ int problem_build(const ps_problem_desc *d, int device, ps_problem *pr) {
     pr->simple = mesh && P.n_cls > 0 && P.n_kinds == 1;
     pr->wide = P.n_slots >= 4096 || getenv("PS_FORCE_WIDE") != nullptr;
     // delta snapshots of wide problems also hold the back ready set (up to 1024 entries)
-    P.snap_b = pr->wide ? std::min(overflow_cap(P.n_slots), 1024) : 0;
+    {
+      int sbc = 1024;
+      if (const char *e = getenv("PS_SNAP_BACK")) sbc = std::max(0, atoi(e));
+      P.snap_b = pr->wide ? std::min(overflow_cap(P.n_slots), sbc) : 0;
+    }
     std::vector<short> l16((size_t)P.n_dev * P.n_dev);
     for (size_t i = 0; i < l16.size(); ++i) {
       int li = d->link_of[i];
