@@ -65,7 +65,7 @@ def parse():
                     help="CPU arm: proposals per chain, the window the GPU chains cover in the default bench")
     ap.add_argument("--py-ref-seconds", type=float, default=8.0,
                     help="wall time of the Python-reference leg (0: skip)")
-    ap.add_argument("--extra", default="alexnet,resnet,nmt,random1k,random10k",
+    ap.add_argument("--extra", default="inception-forward,alexnet,resnet,nmt,random1k,random10k",
                     help="other BASELINE configs measured after the headline ('none': skip)")
     return ap.parse_args()
 
@@ -362,6 +362,7 @@ def timed_steps(ch, h, stream, sh, steps, budget_ns, proposals, flush):
 
 
 EXTRA = {  # name: (chains, step budget ms, distinct starts or None, trace samples)
+    "inception-forward": (1024, 100.0, None, 16),  # the headline workload in forward mode
     "alexnet": (1024, 100.0, None, 16),
     "resnet": (1024, 100.0, None, 8),
     "nmt": (4096, 300.0, 64, 4),
@@ -372,6 +373,8 @@ EXTRA = {  # name: (chains, step budget ms, distinct starts or None, trace sampl
 
 def measure_extra(name, mode, device, stream, sh, flush, peak, steps=3, warmup=2):
     C, bms, distinct, samples = EXTRA[name]
+    if name.endswith("-forward"):
+        name, mode = name[:-len("-forward")], "forward"
     ch = Chains(name, mode, C, 0, True, device, distinct=distinct)
     budget_ns = int(bms * 1e6)
     for _ in range(warmup):
