@@ -377,7 +377,7 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15
 
 // per-warp phase counters of -DPS_PHASES builds (16 bytes otherwise)
 #ifdef PS_PHASES
-#define PH_N 32
+#define PH_N 40
 #else
 #define PH_N 2
 #endif
@@ -520,6 +520,7 @@ struct W2 {
   // "two-level ready set" at warp_simulate2.  bcap == 0: no back set.
   REnt *bq;
   int *bmem;
+  unsigned long long *bh;  // bq[i].h mirrored: the refill's passes read 8 bytes per entry, not 32
   int bcap;
   double *opmin;  // optional [n_ops]: earliest end of each op's forward tasks (exhaustive bounds)
   const TraceSink *tr;  // optional: record every task and dependency (API materialisation)
@@ -617,6 +618,7 @@ __device__ inline void carve_warp(char *base, const DevProb &P, const Lay &L, W2
   w.rcap = P.cap;
   w.bq = nullptr;
   w.bmem = nullptr;
+  w.bh = nullptr;
   w.bcap = 0;
   w.opmin = nullptr;
   w.tr = nullptr;
@@ -635,7 +637,7 @@ __host__ __device__ inline int overflow_cap(int n_slots) { return 4 * n_slots + 
 
 __host__ __device__ inline size_t gscratch_bytes(int n_slots, int n_queues) {
   return al16((size_t)n_slots * 3 * 8) + al16((size_t)n_slots * 3 * 2) + al16((size_t)n_slots) +
-         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + (size_t)overflow_cap(n_slots) * 36 + 256;
+         al16((size_t)n_slots * 8) + al16((size_t)n_queues * 16) + (size_t)overflow_cap(n_slots) * 44 + 256;
 }
 
 // one warp's global slice: scratch, plus its whole shared-memory layout in global mode
@@ -691,6 +693,7 @@ __device__ inline void bind_bids(const DevProb &P, char *gscratch, W2 &w) {
   w.bcap = overflow_cap(P.n_slots);
   w.bq = (REnt *)b;
   w.bmem = (int *)(w.bq + w.bcap);
+  w.bh = (unsigned long long *)(w.bmem + w.bcap);  // (36 bcap: 16-byte aligned, bcap = 4 n + 1024)
 }
 
 // Ready set in the warp's global slice (exact overflow path for wide candidates).
@@ -703,6 +706,7 @@ __device__ inline W2 with_global_ready_set(const DevProb &P, char *gscratch, W2 
   w.rcap = c;
   w.bq = nullptr;  // (the front set now occupies the back set's slice)
   w.bmem = nullptr;
+  w.bh = nullptr;
   w.bcap = 0;
   return w;
 }
@@ -790,7 +794,7 @@ __device__ __forceinline__ bool push2(bool want, double ready, unsigned long lon
       REnt r;
       r.h = hb; r.k = key; r.e = exe; r.q = q; r.pad = 0;
       if (pos < room) w.rs[n + pos] = r;
-      else w.bq[nb + pos - room] = r;
+      else { w.bq[nb + pos - room] = r; w.bh[nb + pos - room] = hb; }
     }
     minb = min(minb, warp_min64(want && pos >= room ? hb : ~0ull, lane));
     n += room;
@@ -1110,7 +1114,7 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
 #pragma unroll 4
   for (int base = 0; base < nb; base += 32) {
     int i = base + lane;
-    unsigned long long h = i < nb ? w.bq[i].h : ~0ull;
+    unsigned long long h = i < nb ? w.bh[i] : ~0ull;
     bool mv = h < X;
     unsigned bm = __ballot_sync(FULLMASK, mv);
     int pos = cnt + __popc(bm & lt);
@@ -1136,7 +1140,11 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
       int t = tb + lane;
       bool surv = t < cnt && !((mask[t >> 5] >> (t & 31)) & 1u);
       unsigned bs = __ballot_sync(FULLMASK, surv);
-      if (surv) w.bq[idx[carry + __popc(bs & lt)]] = w.bq[nb2 + t];  // (holes < nb2 <= survivors)
+      if (surv) {  // (holes < nb2 <= survivors)
+        const int d = idx[carry + __popc(bs & lt)];
+        w.bq[d] = w.bq[nb2 + t];
+        w.bh[d] = w.bh[nb2 + t];
+      }
       carry += __popc(bs);
     }
     n += cnt;
@@ -1164,7 +1172,7 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
       __syncwarp();
       for (int base = 0; base < nb; base += 32) {
         int i = base + lane;
-        unsigned long long h = i < nb ? w.bq[i].h : ~0ull;
+        unsigned long long h = i < nb ? w.bh[i] : ~0ull;
         int b = 0;  // first boundary above h (when h < hiX)
 #pragma unroll
         for (int st = 16; st >= 1; st >>= 1) {
@@ -1207,6 +1215,7 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
     if (mv) w.rs[n + __popc(bm & lt)] = e;
     if (kp) {
       w.bq[kept + __popc(bk & lt)] = e;
+      w.bh[kept + __popc(bk & lt)] = e.h;
       mb = e.h < mb ? e.h : mb;
     }
     n += __popc(bm);
@@ -1269,7 +1278,7 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
     bool ev = v2 && e.h >= T, kp = v2 && !ev;
     unsigned be = __ballot_sync(FULLMASK, ev), bk = __ballot_sync(FULLMASK, kp);
     __syncwarp();
-    if (ev) w.bq[nb + __popc(be & lt)] = e;
+    if (ev) { w.bq[nb + __popc(be & lt)] = e; w.bh[nb + __popc(be & lt)] = e.h; }
     if (kp) w.rs[kept + __popc(bk & lt)] = e;
     nb += __popc(be);
     kept += __popc(bk);
@@ -1288,6 +1297,7 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
     if (!back_refill(w, n, nb, minb, X_, lane)) pend_bslow = true;                           \
     refilled = true;                                                                         \
     PH_CNT(21, 1);                                                                           \
+    PH_ADD(32, t_sel);                                                                       \
     continue;                                                                                \
   }
 
@@ -1452,7 +1462,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     for (int i = lane; i < n + nb; i += 32) {
       REnt r = i < n ? rso[i] : rbo[i - n];
       if (i < n) w.rs[i] = r;
-      else w.bq[i - n] = r;
+      else { w.bq[i - n] = r; w.bh[i - n] = r.h; }
       // a ready op task has no remaining count (the snapshots' "has run" test
       // reads it: ran = no remaining count and not in the ready set)
       unsigned kd = key_kind(r.k);
@@ -1522,6 +1532,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     // not fit, the round restarts over both sets in the back set (bslow).  An
     // empty front set refills against the back set's own LB here.
     bool bslow = false;
+    PH_T(t_rf);
     if (BACK && nb > 0 && (n == 0 || pend_bslow)) {
       bool moved = false;
       if (!pend_bslow) {
@@ -1532,7 +1543,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       if (!moved) {
         if (nb + n > w.bcap) { out.status = PS_STATUS_CAPACITY; return out; }
-        for (int i = lane; i < n; i += 32) w.bq[nb + i] = w.rs[i];
+        for (int i = lane; i < n; i += 32) { REnt r = w.rs[i]; w.bq[nb + i] = r; w.bh[nb + i] = r.h; }
         nb += n;
         n = 0;
         bslow = true;
@@ -1540,6 +1551,7 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       pend_bslow = false;
     }
+    PH_ADD(33, t_rf);
     int sel_base = 0, sel_n = bslow ? 33 : n, rest = 0;
     bool forced = false;
     if (!bslow && n > 32 && n <= 64 && n + 32 <= w.rcap) {
@@ -1750,7 +1762,12 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
       }
       mine = lane < nw;
       w.wlane[lane] = lane;
-      if (bslow) { nb = sn; minb = minready; }  // (the earliest ready time before the round: a lower bound)
+      if (bslow) {  // (minb: the earliest ready time before the round, a lower bound)
+        nb = sn;
+        minb = minready;
+        for (int i = lane; i < nb; i += 32) w.bh[i] = w.bq[i].h;  // the keys of the rewritten back set
+        __syncwarp();
+      }
       else n = sn;
       PH_ADD(19, t_slow);
       PH_CNT(18, nw);
@@ -2001,7 +2018,10 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     refilled = false;
     // keep the front set small: past 64 entries, the later ones move to the back set
     if (BACK && n > 64 && w.bcap) {
+      PH_T(t_trim);
       if (!front_trim(w, n, nb, minb, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+      PH_ADD(30, t_trim);
+      PH_CNT(31, 1);
     }
     // (no barrier here: every path above ends with one after its last shared store)
   }
@@ -2520,7 +2540,7 @@ __device__ __forceinline__ void mcmc_chain(const DevProb &P, const Lay &lay, con
   PH_CNT(7, n_it);
 #ifdef PS_PHASES
   __syncwarp();
-  if (lane < PH_N) atomicAdd(&g_phase[lane], w.ph[lane]);
+  for (int i = lane; i < PH_N; i += 32) atomicAdd(&g_phase[i], w.ph[i]);
 #endif
   for (int i = lane; i < P.n_ops; i += 32) gmapl[i] = w.mapl[i];
   if (!lay.asg_global)

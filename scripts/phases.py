@@ -16,7 +16,7 @@ distinct = None if cfg in ("inception", "alexnet", "resnet") else 16
 ch = Chains(cfg, mode, C, 0, True, 0, distinct=distinct)
 L = nat.lib()
 L.ps_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_int]
-N = 32
+N = 40
 ph = np.zeros(N, np.uint64)
 nat.check(L.ps_mcmc_run_budget(ch.h, 1 << 30, int(bms * 0.5e6), None), "run")
 nat.check(L.ps_debug_phases(nat.ptr(ph), 1), "phases")
@@ -40,6 +40,10 @@ print(f"snapshots {ph[23]/max(sims,1):.1f}/sim, unusable: back set {100*ph[24]/m
       f"ready set over capacity {100*ph[25]/max(ph[23],1):.1f}%")
 print(f"init: in-degrees {ph[26]/max(sims,1):.0f} cycles/sim, restore or seed {ph[27]/max(sims,1):.0f} cycles/sim")
 print(f"snapshot writes {ph[28]/max(sims,1):.0f} cycles/sim, delta_prepare {ph[29]/max(sims,1):.0f} cycles/sim")
+print(f"front trims {100*ph[31]/max(rounds,1):.1f}% of rounds, {ph[30]/max(ph[31],1):.0f} cycles each, "
+      f"{ph[30]/max(rounds,1):.0f} cycles/round")
+print(f"restarted selections (refill from BACK_CHECK) {ph[32]/max(rounds,1):.0f} cycles/round; "
+      f"round-start refills / combined slow set-up {ph[33]/max(rounds,1):.0f} cycles/round")
 tot = ph[6]
 for i in (0, 1, 2, 5, 15, 19, 3, 4):
     print(f"{names[i]:12s} {ph[i]/max(sims,1):12.0f} cycles/sim  {100*ph[i]/max(tot,1):5.1f}% of loop   "
