@@ -1232,6 +1232,51 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
 // T move to the back set, whose bound becomes min(minb, T).  Any T is exact
 // (only the split changes).
 __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigned long long &minb, int lane) {
+#ifdef PS_TRIM_HIST
+  // threshold from a 32-bin histogram of the front's ready times between their
+  // minimum and maximum: the largest boundary that keeps 1..48 entries (else the
+  // first boundary that keeps any)
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int i = lane; i < n; i += 32) {
+    const unsigned long long h = w.rs[i].h;
+    lo = h < lo ? h : lo;
+    hi = h > hi ? h : hi;
+  }
+  lo = warp_min64(lo, lane);
+  hi = ~warp_min64(~hi, lane);
+  if (lo == hi) return true;  // (all tied: keep everything)
+  unsigned long long bj;
+  {
+    const double dl = __longlong_as_double((long long)lo), dh = __longlong_as_double((long long)hi);
+    bj = lane == 31 ? hi : (unsigned long long)__double_as_longlong(dl + (dh - dl) * ((double)(lane + 1) * 0.03125));
+    bj = bj < hi ? bj : hi;
+  }
+  int *hist = w.wlane;  // (32 ints, free until the next round picks its winners)
+  hist[lane] = 0;
+  __syncwarp();
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const unsigned long long h = i < n ? w.rs[i].h : ~0ull;
+    int b = 0;  // first boundary above h (when h < hi)
+#pragma unroll
+    for (int st = 16; st >= 1; st >>= 1) {
+      unsigned long long x = __shfl_sync(FULLMASK, bj, b + st - 1);
+      if (!(h < x)) b += st;
+    }
+    if (h < hi) atomicAdd(&hist[b], 1);
+  }
+  __syncwarp();
+  int c = hist[lane];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int y = __shfl_up_sync(FULLMASK, c, off);
+    if (lane >= off) c += y;
+  }
+  const unsigned okm = __ballot_sync(FULLMASK, c >= 1 && c <= 48), anym = __ballot_sync(FULLMASK, c >= 1);
+  const int jb = okm ? 31 - __clz(okm) : __ffs(anym) - 1;  // (anym != 0: lo < bj[31] = hi)
+  const unsigned long long T = __shfl_sync(FULLMASK, bj, jb);
+  __syncwarp();
+#else
   unsigned long long v[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -1264,6 +1309,7 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
   }
   const unsigned long long T = __shfl_sync(FULLMASK, v[1], 0), lo = __shfl_sync(FULLMASK, v[0], 0);
   if (T == lo) return true;  // (ties at the minimum: keep everything)
+#endif
   int evict = 0;
   for (int i = lane; i < n; i += 32) evict += w.rs[i].h >= T ? 1 : 0;
   evict = (int)__reduce_add_sync(FULLMASK, (unsigned)evict);
