@@ -1231,8 +1231,10 @@ __device__ __forceinline__ bool back_refill(const W2 &w, int &n, int &nb, unsign
 // among the first 128 (bitonic sort, four per lane); entries ready at or after
 // T move to the back set, whose bound becomes min(minb, T).  Any T is exact
 // (only the split changes).
-__device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigned long long &minb, int lane) {
-#ifdef PS_TRIM_HIST
+__device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigned long long &minb, int lane,
+                                           bool by_hist) {
+  unsigned long long T;
+  if (by_hist) {
   // threshold from a 32-bin histogram of the front's ready times between their
   // minimum and maximum: the largest boundary that keeps 1..48 entries (else the
   // first boundary that keeps any)
@@ -1274,9 +1276,9 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
   }
   const unsigned okm = __ballot_sync(FULLMASK, c >= 1 && c <= 48), anym = __ballot_sync(FULLMASK, c >= 1);
   const int jb = okm ? 31 - __clz(okm) : __ffs(anym) - 1;  // (anym != 0: lo < bj[31] = hi)
-  const unsigned long long T = __shfl_sync(FULLMASK, bj, jb);
+  T = __shfl_sync(FULLMASK, bj, jb);
   __syncwarp();
-#else
+  } else {
   unsigned long long v[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -1307,9 +1309,10 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
       }
     }
   }
-  const unsigned long long T = __shfl_sync(FULLMASK, v[1], 0), lo = __shfl_sync(FULLMASK, v[0], 0);
+  T = __shfl_sync(FULLMASK, v[1], 0);
+  const unsigned long long lo = __shfl_sync(FULLMASK, v[0], 0);
   if (T == lo) return true;  // (ties at the minimum: keep everything)
-#endif
+  }
   int evict = 0;
   for (int i = lane; i < n; i += 32) evict += w.rs[i].h >= T ? 1 : 0;
   evict = (int)__reduce_add_sync(FULLMASK, (unsigned)evict);
@@ -1349,6 +1352,7 @@ __device__ __forceinline__ bool front_trim(const W2 &w, int &n, int &nb, unsigne
 
 template <int M>
 __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, const Lay &L, char *gscratch, int lane) {
+  const bool trim_hist = !L.global_all;  // front-trim threshold method (see the trim at the end of a round)
   constexpr bool SIMPLE = (M & SIM_SIMPLE) != 0;  // one device kind, <= 2 link classes, full mesh
   constexpr bool SNAP = (M & SIM_SNAP) != 0;      // delta evaluation: snapshots, first rounds, resume
   constexpr bool BACK = (M & SIM_BACK) != 0;      // wide problems: two-level ready set (front + back)
@@ -2065,7 +2069,16 @@ __device__ SimOut warp_simulate2(const DevProb &P, const Tab &T, const W2 &w, co
     // keep the front set small: past 64 entries, the later ones move to the back set
     if (BACK && n > 64 && w.bcap) {
       PH_T(t_trim);
-      if (!front_trim(w, n, nb, minb, lane)) { out.status = PS_STATUS_CAPACITY; return out; }
+      // threshold: a histogram of the front's ready times where the tables sit on
+      // chip (NMT-40 +8 %, random-1k +5 %), the 33rd smallest by a bitonic sort in
+      // the all-global layout (random-10k: the histogram's smaller fronts refill
+      // more often, -8 %); PS_TRIM_HIST=0/1 at build time forces one
+#ifdef PS_TRIM_HIST
+      const bool by_hist = PS_TRIM_HIST != 0;
+#else
+      const bool by_hist = trim_hist;
+#endif
+      if (!front_trim(w, n, nb, minb, lane, by_hist)) { out.status = PS_STATUS_CAPACITY; return out; }
       PH_ADD(30, t_trim);
       PH_CNT(31, 1);
     }
